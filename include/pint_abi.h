@@ -1,0 +1,209 @@
+/*
+ * pint_abi.h — C ABI of the B200-native Parareal hot path.
+ *
+ * This is the drop-in boundary for the reference's propagator plugin layer
+ * and its synchronous sweep. Every entry point is extern "C", takes plain
+ * pointers and sizes, and never exposes torch or CUDA C++ types. The
+ * reference is pure Python (pintlab); the Python-side binding that a
+ * maintainer would add is the ctypes stub shown in INTEGRATION.md.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/pintlab):
+ *   pint_op_create          <- PROPAGATOR_RULES builders
+ *                              backward_euler_propagator   model.py:172-184
+ *                              trapezoidal_propagator      model.py:187-200
+ *                              fine_from_onestep (explicit) model.py:147-154
+ *                              _onestep + lu_solve          model.py:157-169, linalg.py:241-266
+ *   pint_op_apply_batch     <- AffinePropagator.apply       model.py:123-129
+ *                              (batched over independent time slices)
+ *   pint_correct            <- parareal_update              parareal.py:25-36
+ *                              + (new - prev).max_abs()     parareal.py:126, linalg.py:113-117
+ *                              + finiteness check           linalg.py:74-75
+ *   pint_coarse_init        <- coarse_init                  parareal.py:54-63
+ *   pint_sync_sweep         <- one sweep of run_parareal    parareal.py:119-127
+ *                              (frozen prefix, F-only branch, delta)
+ *   pint_async_run          <- run_async_parareal           async_parareal.py:61-84
+ *                              (real concurrency instead of the
+ *                               simulate_async event loop, async_engine.py:238-365)
+ *
+ * Error codes map onto the reference's exception taxonomy (errors.py):
+ *   PINT_EDIM       -> DimensionError                errors.py:10-11
+ *   PINT_EARG       -> ValueError
+ *   PINT_ENONFINITE -> ValueError("... must be finite") linalg.py:74-75
+ *   PINT_ENOCONV    -> ConvergenceFailure(estimate)  errors.py:18-26
+ *   PINT_ESINGULAR  -> SingularSystemError(dt, pivot) errors.py:37-43
+ *   PINT_ECUDA      -> RuntimeError(cuda error string)
+ *   PINT_EUNSUPPORTED -> NotImplementedError
+ * The message of the last error on a context is returned by pint_last_error.
+ *
+ * Threading: all compute calls are stream-ordered and asynchronous with
+ * respect to the host unless stated. A context is bound to one device and is
+ * not thread-safe. Operators are immutable after creation; all scratch is
+ * allocated at creation (no allocation inside hot calls).
+ */
+#ifndef PINT_ABI_H
+#define PINT_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PINT_ABI_VERSION 1
+
+enum pint_status {
+  PINT_OK = 0,
+  PINT_EDIM = 1,
+  PINT_EARG = 2,
+  PINT_ENONFINITE = 3,
+  PINT_ENOCONV = 4,
+  PINT_ESINGULAR = 5,
+  PINT_ECUDA = 6,
+  PINT_EUNSUPPORTED = 7
+};
+
+enum pint_dtype { PINT_F32 = 0, PINT_F64 = 1 };
+
+enum pint_rule {
+  PINT_RULE_BACKWARD_EULER = 0, /* (I - dt A) u+ = u + dt c                */
+  PINT_RULE_TRAPEZOIDAL = 1,    /* (I - dt/2 A) u+ = (I + dt/2 A) u + dt c */
+  PINT_RULE_FORWARD_EULER = 2   /* u+ = (I + dt A) u + dt c               */
+};
+
+typedef struct pint_ctx pint_ctx;
+typedef struct pint_op pint_op;
+
+/*
+ * Operator description. The operator is u' = A u + c on a tensor grid of
+ * ndim (1..3) axes, shape[d] interior points per axis.
+ *   ndim == 1: A = a_diag * I + a_off * (S + S^T) (symmetric constant-coefficient
+ *              tridiagonal; heat1d_system gives a_diag = -2/h^2, a_off = 1/h^2;
+ *              scalar_decay_system gives n = 1, a_diag = -rate), and the
+ *              forcing c is nonzero only at the end nodes: c[0] = c_first,
+ *              c[n-1] = c_last (summed when n == 1).
+ *   ndim >= 2: A = (1/h^2) * (zero-Dirichlet 5/7-point Laplacian), c = 0.
+ * One propagator application advances `steps` steps of width dt = span/steps.
+ * Implicit rules in 2-D/3-D are solved by conjugate gradients to
+ * ||r||_2 <= cg_rtol * ||b||_2 (at most cg_maxit iterations).
+ */
+typedef struct pint_op_desc {
+  int32_t ndim;
+  int32_t rule;      /* enum pint_rule */
+  int32_t dtype;     /* enum pint_dtype */
+  int32_t reserved0;
+  int64_t shape[3];
+  double h;          /* grid spacing (ndim >= 2) */
+  double span;       /* time covered by one application */
+  int64_t steps;     /* steps per application (>= 1) */
+  double a_diag;     /* ndim == 1 */
+  double a_off;      /* ndim == 1 */
+  double c_first;    /* ndim == 1 */
+  double c_last;     /* ndim == 1 */
+  double cg_rtol;    /* ndim >= 2 implicit */
+  int64_t cg_maxit;  /* ndim >= 2 implicit */
+  int32_t layout_ch; /* 0 = auto; else points per thread (1-D: 16 or 32) */
+  int32_t reserved1;
+} pint_op_desc;
+
+/* Static facts about a created operator (for cost models and benchmarks). */
+typedef struct pint_op_info {
+  int64_t dim;             /* points per state */
+  int64_t steps;
+  int32_t dtype;
+  int32_t rule;
+  int32_t threads_per_slice;   /* 1-D: T = 32 * warps */
+  int32_t points_per_thread;   /* 1-D: CH */
+  int32_t batch_cluster;       /* CTAs per slice in apply_batch */
+  int32_t sweep_cluster;       /* CTAs in the fused coarse sweep */
+  double dt;
+  double diag;                 /* 1-D: D of the implicit step matrix */
+  double offdiag;              /* 1-D: E of the implicit step matrix */
+  double min_pivot;
+} pint_op_info;
+
+int pint_abi_version(void);
+
+int pint_ctx_create(int device, pint_ctx **out);
+int pint_ctx_destroy(pint_ctx *ctx);
+const char *pint_last_error(const pint_ctx *ctx);
+/* Estimate payload of the last PINT_ENOCONV / pivot of the last PINT_ESINGULAR. */
+double pint_last_error_value(const pint_ctx *ctx);
+
+int pint_op_create(pint_ctx *ctx, const pint_op_desc *desc, pint_op **out);
+int pint_op_destroy(pint_op *op);
+int pint_op_get_info(const pint_op *op, pint_op_info *info);
+
+/*
+ * out[b] = P(in[b]) for b in [0, nbatch): in/out are device pointers to
+ * nbatch states of `dim` elements, consecutive states `stride` elements
+ * apart. in and out must not alias. Stream-ordered on `stream`
+ * (a cudaStream_t, NULL = legacy default stream).
+ */
+int pint_op_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
+                        int64_t stride, void *stream);
+
+/*
+ * Predictor-corrector update, elementwise over nbatch states of dim points:
+ *   out = f_only[b] ? f : (gnew + f) - gold         (parareal.py:34-36)
+ *   delta[b] = max |out - prev|                       (parareal.py:126)
+ * f_only may be NULL (all zero). prev may be NULL (no delta). delta_dev is a
+ * device array of nbatch doubles; *nonfinite_dev (device int32) is set to 1
+ * when any output is NaN/Inf (never cleared by this call).
+ */
+int pint_correct(pint_ctx *ctx, int32_t dtype, int64_t dim, int64_t nbatch,
+                 const void *gnew, const void *f, const void *gold,
+                 const void *prev, void *out, const uint8_t *f_only,
+                 double *delta_dev, int32_t *nonfinite_dev, void *stream);
+
+/*
+ * lam[i] = G(lam[i-1]) for i = 1..p, lam is (p+1) x dim contiguous with
+ * lam[0] = u0 preset. If gcache != NULL it receives a copy of lam (G of the
+ * coarse initial iterate, i.e. G(lam[i-1]) at row i) for the first sweep.
+ */
+int pint_coarse_init(pint_op *coarse, void *lam, int64_t p, void *gcache,
+                     void *stream);
+
+/*
+ * One synchronous sweep k (1 <= k <= p) of run_parareal, given fv[i] =
+ * F(prev[i-1]) for i in [k, p] (rows of a (p+1) x dim array):
+ *   next[i] = prev[i]                       for i < k (caller-owned copy; the
+ *                                           call writes next[k-1] itself)
+ *   next[i] = F-only ? fv[i] : (G(next[i-1]) + fv[i]) - gcache[i]   for i >= k
+ *   gcache[i] <- G(next[i-1])               for i >= k (the next sweep's G(old))
+ *   deltas_dev[i] = max |next[i] - prev[i]| for i >= k, 0 for i = k-1
+ * The F-only branch fires when deltas_dev[i-1] == 0 (bitwise-equal readings;
+ * always at i == k). *nonfinite_dev is set to 1 on any non-finite output.
+ * coarse must be the same operator that produced gcache.
+ */
+int pint_sync_sweep(pint_op *coarse, const void *prev, void *next,
+                    const void *fv, void *gcache, int64_t k, int64_t p,
+                    double *deltas_dev, int32_t *nonfinite_dev, void *stream);
+
+/*
+ * *equal_dev (device uint8) <- 1 if a[i] == b[i] for all i < dim (IEEE
+ * equality: -0.0 == 0.0, NaN != NaN — numpy.array_equal semantics, the
+ * F-only test of parareal.py:34), else 0.
+ */
+int pint_equal_flag(pint_ctx *ctx, int32_t dtype, int64_t dim, const void *a,
+                    const void *b, uint8_t *equal_dev, void *stream);
+
+/* max over deltas_dev[lo..hi) -> *out_dev (device double), deterministic. */
+int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,
+                    int64_t hi, double *out_dev, void *stream);
+
+/*
+ * Host-only export of the exact 1-D solver plan a backward-Euler /
+ * trapezoidal operator would use (no device needed): dims_out[0..5] =
+ * {CH, T, nW, J, tb, NF}; fac_out = 10*CH doubles (regular then tail chunk:
+ * q, e, h, w, ws); table_out = NF*T doubles ([field][thread]); scal_out =
+ * {D, E, f_first, f_last, fq_first, fq_last, t_last, l_last}. Pass NULL
+ * buffers to query dims only. Used by the CPU tests to emulate the kernel.
+ */
+int pint_tri1d_plan_host(const pint_op_desc *desc, int32_t *dims_out,
+                         double *fac_out, double *table_out, double *scal_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PINT_ABI_H */

@@ -1,0 +1,178 @@
+"""Asynchronous Parareal (reference: pintlab/async_parareal.py:1-84).
+
+Worker i owns interface state i. On activation it reads its predecessor
+twice: slot 1 (FRESH) takes the freshest version the schedule lets it see,
+slot 2 (REMEMBERED) replays the version it consumed through slot 1 at its
+previous activation (default version 0 = the coarse initial value). When the
+two readings coincide bitwise the update collapses to F(remembered), which
+drives finite termination.
+
+``run_async_parareal`` keeps the reference's deterministic event semantics
+(same seeds -> same activation order, staleness draws, reads and values) with
+the state, the version-stamped retention buffers and every evaluation
+(F, G, the equality test, the correction and the delta) on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+from collections import deque
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .async_engine import (
+    STOP_PREDICATE,
+    STOP_QUIESCENCE,
+    AsyncSchedule,
+    AsyncTrace,
+    EngineView,
+    ScheduleDriver,
+    UpdateRecord,
+)
+from .errors import HorizonExhausted
+from .linalg import BlockVector
+from .parareal import _coarse_init_into, _u0_tensor, correct_into
+
+FRESH_SLOT = 1
+REMEMBERED_SLOT = 2
+PERSISTENT_SLOTS = {REMEMBERED_SLOT: FRESH_SLOT}
+SNAPSHOT_LIMIT_BYTES = 1 << 30
+
+
+def async_stop_check(worker_deltas, epsilon: float, drained: bool) -> bool:
+    """Every worker's last change strictly below epsilon and no newer version
+    still unseen by its consumer (async_parareal.py:52-58)."""
+    if epsilon <= 0.0:
+        raise ValueError(f"epsilon must be positive, got {epsilon}")
+    deltas = np.asarray(worker_deltas, dtype=float)
+    return bool(drained and float(np.max(deltas)) < epsilon)
+
+
+class _Evaluator:
+    """parareal_update on device buffers with a device-side F-only flag."""
+
+    def __init__(self, coarse, fine):
+        self.coarse, self.fine = coarse, fine
+        dev = f"cuda:{fine.device}"
+        n = fine.dim
+        self.gf = torch.empty(1, n, dtype=fine.dtype, device=dev)
+        self.go = torch.empty_like(self.gf)
+        self.fo = torch.empty_like(self.gf)
+        self.eq = torch.zeros(1, dtype=torch.uint8, device=dev)
+        self.delta = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.lib = _native.load_library()
+        self.dt = _native.PINT_F64 if fine.dtype == torch.float64 else _native.PINT_F32
+
+    def __call__(self, fresh: torch.Tensor, rem: torch.Tensor, same_version: bool, prev: torch.Tensor,
+                 out: torch.Tensor) -> None:
+        n = self.fine.dim
+        self.fine.apply_ptr(rem.data_ptr(), self.fo.data_ptr(), 1, n)
+        if same_version:
+            self.eq.fill_(1)
+        else:
+            s = ctypes.c_void_p(_device.stream_ptr(self.fine.device))
+            rc = self.lib.pint_equal_flag(self.fine._ctx.handle, self.dt, n, ctypes.c_void_p(fresh.data_ptr()),
+                                          ctypes.c_void_p(rem.data_ptr()), ctypes.c_void_p(self.eq.data_ptr()), s)
+            _native.check(rc, self.fine._ctx.handle, "pint_equal_flag")
+            self.coarse.apply_ptr(fresh.data_ptr(), self.gf.data_ptr(), 1, n)
+            self.coarse.apply_ptr(rem.data_ptr(), self.go.data_ptr(), 1, n)
+        correct_into(self.fine, self.gf, self.fo, self.go, prev.reshape(1, -1), out.reshape(1, -1), self.eq,
+                     self.delta, self.flag, 1)
+
+
+def simulate_parareal_async(coarse, fine, init: torch.Tensor, schedule: AsyncSchedule, stop=None,
+                            record_snapshots: bool = True, record_digests: bool | None = None) -> AsyncTrace:
+    """Event loop of async_engine.py:238-365 specialised to the two-slot
+    Parareal mapping (async_parareal.py:24-49), evaluated on the GPU."""
+    p = init.shape[0] - 1
+    n = init.shape[1]
+    bound = schedule.delay_bound
+    window = schedule.window(p)
+    driver = ScheduleDriver(schedule, p)
+    esz = init.element_size()
+    if record_snapshots and (p + 1) * n * esz * min(schedule.max_events, 4096) > SNAPSHOT_LIMIT_BYTES:
+        record_snapshots = False
+    if record_digests is None:
+        record_digests = n <= 4096
+    state = init.clone()
+    versions = [0] * (p + 1)
+    buffers = [deque([(0, init[i].clone())], maxlen=bound + 1) for i in range(p + 1)]
+    remembered: dict = {}
+    consumed: dict = {}
+    last = np.full(p + 1, np.inf)
+    last[0] = 0.0
+    counts = np.zeros(p + 1, dtype=int)
+    events, snapshots = [], []
+    zero_streak = 0
+    quiescent_streak = (bound + 3) * window
+    stop_reason = None
+    ev = _Evaluator(coarse, fine)
+    for k in range(schedule.max_events):
+        comp = driver.next_component(k)
+        src = comp - 1
+        staleness = driver.sample_staleness()
+        vf = max(versions[src] - staleness, 0)
+        buf = buffers[src]
+        idx = len(buf) - 1 - (buf[-1][0] - vf)
+        if idx < 0:
+            raise KeyError(f"version {vf} already evicted from the retention buffer")
+        fresh = buf[idx][1]
+        vr, rem = remembered.get(comp, (0, init[src]))
+        consumed[comp] = vf
+        new = torch.empty_like(state[comp])
+        ev(fresh, rem, vr == vf, state[comp], new)
+        delta = float(ev.delta.item())
+        if bool(ev.flag.item()):
+            raise ValueError("block entries must be finite")
+        state[comp].copy_(new)
+        versions[comp] += 1
+        buffers[comp].append((versions[comp], new))
+        counts[comp] += 1
+        last[comp] = delta
+        remembered[comp] = (vf, fresh)
+        digest = hashlib.sha256(_device.to_host(new).tobytes()).hexdigest()[:16] if record_digests else ""
+        events.append(UpdateRecord(k_global=k, component=comp,
+                                   reads=((src, FRESH_SLOT, vf), (src, REMEMBERED_SLOT, vr)),
+                                   digest=digest, delta=delta))
+        if record_snapshots:
+            snapshots.append(BlockVector(state.clone(), check_finite=False))
+        zero_streak = zero_streak + 1 if delta == 0.0 else 0
+        if zero_streak >= quiescent_streak:
+            stop_reason = STOP_QUIESCENCE
+            break
+        if stop is not None:
+            drained = all(consumed.get(i) == versions[i - 1] for i in range(1, p + 1))
+            if stop(EngineView(k, BlockVector(state, check_finite=False), last.copy(), drained)):
+                stop_reason = STOP_PREDICATE
+                break
+    trace = AsyncTrace(events=events, snapshots=snapshots, initial=BlockVector(init.clone(), check_finite=False),
+                       per_component_counts=counts, stop_event=len(events) - 1, stop_reason=stop_reason or "",
+                       schedule=schedule, n_updatable=p, persistent_slots=dict(PERSISTENT_SLOTS),
+                       final=BlockVector(state.clone(), check_finite=False))
+    if stop_reason is None:
+        raise HorizonExhausted(f"no stop condition met within {schedule.max_events} events", trace)
+    return trace
+
+
+def run_async_parareal(coarse, fine, u0, p: int, schedule: AsyncSchedule, epsilon: float | None = None,
+                       record_snapshots: bool = True) -> AsyncTrace:
+    """Asynchronous iteration from the coarse initialization
+    (async_parareal.py:61-84). With epsilon, stops once all per-worker last
+    changes are strictly below it and the read edges are drained; with
+    epsilon None it runs to exact quiescence."""
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+    init = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")
+    init[0] = _u0_tensor(coarse, u0)
+    _coarse_init_into(coarse, init, p, None)
+    stop = None
+    if epsilon is not None:
+        eps = float(epsilon)
+
+        def stop(view: EngineView) -> bool:
+            return async_stop_check(view.last_deltas[1:], eps, view.drained)
+
+    return simulate_parareal_async(coarse, fine, init, schedule, stop=stop, record_snapshots=record_snapshots)

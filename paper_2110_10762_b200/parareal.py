@@ -1,0 +1,280 @@
+"""Synchronous Parareal on the B200 (reference: pintlab/parareal.py:1-138).
+
+Same names, signatures, stop rules and results as the reference:
+
+* ``parareal_update`` — G(fresh) + F(old) - G(old) in that FP order, or
+  F(old) when the two readings are bitwise equal (parareal.py:25-36);
+* ``sequential_fine_solve`` / ``coarse_init`` (parareal.py:39-63);
+* ``parareal_iterate`` — one full sweep, no freeze (parareal.py:66-76);
+* ``run_parareal`` — frozen prefix, strict threshold, stop order
+  threshold -> exact -> k_max (parareal.py:99-138).
+
+The hot loop is restructured for the GPU without changing any value:
+each sweep is one batched launch of F over all live slices (the F calls of a
+sweep are independent, parareal.py:125) followed by one fused coarse-sweep
+launch that carries the running iterate on-chip through the serial G chain and
+applies the correction and the per-slice convergence norm in its epilogue
+(pint_sync_sweep). G(old) is not recomputed: it is the previous sweep's
+G(new) of the same bits (Algorithm 1's w_i^k).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .linalg import BlockVector
+
+STOP_THRESHOLD = "threshold"
+STOP_KMAX = "k_max"
+STOP_EXACT = "exact"
+
+RECORD_LIMIT_BYTES = 1 << 30  # keep every iterate only while they fit in 1 GiB
+
+
+def _ctx(prop):
+    return prop._ctx.handle
+
+
+def _stream(prop):
+    return ctypes.c_void_p(_device.stream_ptr(prop.device))
+
+
+def correct_into(ctx_prop, gnew, f, gold, prev, out, f_only, delta, nonfinite, nbatch: int) -> None:
+    """pint_correct on device tensors (rows of length dim)."""
+    lib = _native.load_library()
+    dtype = _native.PINT_F64 if out.dtype == torch.float64 else _native.PINT_F32
+    dim = out.shape[-1]
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None else 0)  # noqa: E731
+    rc = lib.pint_correct(_ctx(ctx_prop), dtype, int(dim), int(nbatch), ptr(gnew), ptr(f), ptr(gold), ptr(prev),
+                          ptr(out), ptr(f_only), ptr(delta), ptr(nonfinite), _stream(ctx_prop))
+    _native.check(rc, _ctx(ctx_prop), "pint_correct")
+
+
+def parareal_update(coarse, fine, fresh_prev, old_prev):
+    """One interface-state correction from two predecessor readings
+    (parareal.py:25-36). Inputs may be numpy arrays or device tensors; the
+    result is of the same kind."""
+    is_torch = isinstance(fresh_prev, torch.Tensor) or isinstance(old_prev, torch.Tensor)
+    dev = fine.device
+    fresh, _ = _device.as_device_tensor(fresh_prev, dev, fine.dtype)
+    old, _ = _device.as_device_tensor(old_prev, dev, fine.dtype)
+    fresh = fresh.reshape(-1)
+    old = old.reshape(-1)
+    if torch.equal(fresh, old):
+        out = fine.apply(old)
+    else:
+        g_f = coarse.apply(fresh)
+        f_o = fine.apply(old)
+        g_o = coarse.apply(old)
+        out = torch.empty_like(f_o)
+        correct_into(fine, g_f, f_o, g_o, None, out, None, None, None, 1)
+    return out if is_torch else _device.to_host(out).astype(float)
+
+
+def _u0_tensor(prop, u0) -> torch.Tensor:
+    t, _ = _device.as_device_tensor(u0, prop.device, prop.dtype)
+    t = t.reshape(-1)
+    if t.numel() != prop.dim:
+        from .errors import DimensionError
+        raise DimensionError(f"initial state has dim {t.numel()}, expected {prop.dim}")
+    return t
+
+
+def sequential_fine_solve(fine, u0, p: int) -> BlockVector:
+    """lambda_0 = u0, lambda_i = F(lambda_{i-1}) (parareal.py:39-51): the
+    purely sequential fine solution every parallel variant must reproduce."""
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+    lam = torch.empty(p + 1, fine.dim, dtype=fine.dtype, device=f"cuda:{fine.device}")
+    lam[0] = _u0_tensor(fine, u0)
+    for i in range(1, p + 1):
+        fine.apply_ptr(lam[i - 1].data_ptr(), lam[i].data_ptr(), 1, fine.dim)
+    return BlockVector(lam, check_finite=False)
+
+
+def _coarse_init_into(coarse, lam: torch.Tensor, p: int, gcache: torch.Tensor | None) -> None:
+    lib = _native.load_library()
+    rc = lib.pint_coarse_init(coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
+                              ctypes.c_void_p(gcache.data_ptr() if gcache is not None else 0), _stream(coarse))
+    _native.check(rc, _ctx(coarse), "pint_coarse_init")
+
+
+def coarse_init(coarse, u0, p: int) -> BlockVector:
+    """Initial interface states from a sequential coarse pass (parareal.py:54-63)."""
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+    lam = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")
+    lam[0] = _u0_tensor(coarse, u0)
+    _coarse_init_into(coarse, lam, p, None)
+    return BlockVector(lam, check_finite=False)
+
+
+def parareal_iterate(coarse, fine, lam: BlockVector) -> BlockVector:
+    """One full sweep over all interface states, ascending in i, component 0
+    pinned (parareal.py:66-76)."""
+    prev = lam.tensor.to(device=f"cuda:{fine.device}", dtype=fine.dtype)
+    p = prev.shape[0] - 1
+    new = prev.clone()
+    fv = fine.apply_batch(prev[:p])
+    g = torch.empty(1, fine.dim, dtype=fine.dtype, device=prev.device)
+    go = torch.empty_like(g)
+    for i in range(1, p + 1):
+        if torch.equal(new[i - 1], prev[i - 1]):
+            new[i] = fv[i - 1]
+            continue
+        coarse.apply_ptr(new[i - 1].data_ptr(), g.data_ptr(), 1, fine.dim)
+        coarse.apply_ptr(prev[i - 1].data_ptr(), go.data_ptr(), 1, fine.dim)
+        correct_into(fine, g, fv[i - 1:i], go, None, new[i:i + 1], None, None, None, 1)
+    return BlockVector(new, check_finite=False)
+
+
+@dataclass
+class SyncTrace:
+    """Record of a synchronous run (parareal.py:79-96). ``iterates`` holds every
+    iterate when they fit in RECORD_LIMIT_BYTES (or record_iterates=True),
+    else only the initial and the final iterate; ``final`` is always the last."""
+
+    iterates: list
+    k_final: int
+    stop_reason: str
+    deltas: list
+    final: BlockVector | None = None
+    slice_deltas: list = field(default_factory=list)
+
+    def to_json(self, include_iterates: bool = False) -> str:
+        doc = {"k_final": self.k_final, "stop_reason": self.stop_reason, "deltas": list(self.deltas)}
+        if include_iterates:
+            doc["iterates"] = [it.data.tolist() for it in self.iterates]
+        return json.dumps(doc, sort_keys=True)
+
+
+class SyncEngine:
+    """Device buffers and launches of the synchronous iteration.
+
+    lam_a / lam_b  ping-pong iterates ((p+1) x dim, HBM resident)
+    fv             F(prev[i-1]) for the live slices of the current sweep
+    gcache         G(prev[i-1]): the previous sweep's G(new), reused as G(old)
+    deltas         per-slice max |new - prev| of the current sweep
+    """
+
+    def __init__(self, coarse, fine, p: int):
+        if coarse.dim != fine.dim:
+            from .errors import DimensionError
+            raise DimensionError("coarse and fine propagators differ in dimension")
+        if coarse.device != fine.device or coarse.dtype != fine.dtype:
+            raise ValueError("coarse and fine propagators must share device and dtype")
+        self.coarse, self.fine, self.p = coarse, fine, int(p)
+        dev = f"cuda:{fine.device}"
+        n = fine.dim
+        self.lam_a = torch.empty(p + 1, n, dtype=fine.dtype, device=dev)
+        self.lam_b = torch.empty_like(self.lam_a)
+        self.fv = torch.empty_like(self.lam_a)
+        self.gcache = torch.empty_like(self.lam_a)
+        self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
+        self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.fonly = torch.zeros(1, dtype=torch.uint8, device=dev)
+        self.host = torch.zeros(2, dtype=torch.float64).pin_memory() if torch.cuda.is_available() else None
+        self.fused = coarse.is_tridiagonal
+        self.prev = self.lam_a
+        self.lib = _native.load_library()
+
+    def init(self, u0) -> None:
+        self.lam_a[0] = _u0_tensor(self.coarse, u0)
+        self.lam_b[0] = self.lam_a[0]
+        _coarse_init_into(self.coarse, self.lam_a, self.p, self.gcache)
+        self.prev = self.lam_a
+        self.flag.zero_()
+
+    def sweep(self, k: int, nxt: torch.Tensor) -> None:
+        """Sweep k (device work only, stream-ordered): nxt <- new iterate."""
+        p, n = self.p, self.fine.dim
+        prev = self.prev
+        self.fine.apply_ptr(prev[k - 1].data_ptr(), self.fv[k].data_ptr(), p - k + 1, n)
+        if self.fused:
+            rc = self.lib.pint_sync_sweep(
+                self.coarse.handle, ctypes.c_void_p(prev.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
+                ctypes.c_void_p(self.fv.data_ptr()), ctypes.c_void_p(self.gcache.data_ptr()), int(k), int(p),
+                ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()),
+                _stream(self.coarse))
+            _native.check(rc, _ctx(self.coarse), "pint_sync_sweep")
+        else:
+            self._generic_sweep(k, nxt)
+        rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, p + 1,
+                                      ctypes.c_void_p(self.dmax.data_ptr()), _stream(self.fine))
+        _native.check(rc, _ctx(self.fine), "pint_max_reduce")
+        self.prev = nxt
+
+    def _generic_sweep(self, k: int, nxt: torch.Tensor) -> None:
+        """Coarse chain + correction for coarse operators without a fused
+        sweep kernel (CG coarse in 2-D/3-D): same values, one launch per slice."""
+        p, prev = self.p, self.prev
+        nxt[k - 1].copy_(prev[k - 1])
+        self.deltas[k - 1] = 0.0
+        g = torch.empty(1, self.fine.dim, dtype=self.fine.dtype, device=nxt.device)
+        for i in range(k, p + 1):
+            self.coarse.apply_ptr(nxt[i - 1].data_ptr(), g.data_ptr(), 1, self.fine.dim)
+            f_only = (i == k) or float(self.deltas[i - 1]) == 0.0
+            self.fonly.fill_(1 if f_only else 0)
+            correct_into(self.fine, g, self.fv[i:i + 1], self.gcache[i:i + 1], prev[i:i + 1], nxt[i:i + 1],
+                         self.fonly, self.deltas[i:i + 1], self.flag, 1)
+            self.gcache[i].copy_(g[0])
+
+    def read_delta(self) -> float:
+        """Host read of the sweep's delta (the one sync per sweep)."""
+        if bool(self.flag.item()):
+            raise ValueError("block entries must be finite")
+        return float(self.dmax.item())
+
+
+def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = None, *,
+                 record_iterates: bool | None = None) -> SyncTrace:
+    """Iterate from the coarse initialization until a stop condition fires
+    (parareal.py:99-138): "threshold" when the sweep-to-sweep change drops
+    strictly below epsilon, "exact" at k == p, "k_max" at the budget.
+    Components i < k are frozen (already exact)."""
+    if epsilon < 0.0:
+        raise ValueError(f"epsilon must be nonnegative, got {epsilon}")
+    cap = p if k_max is None else min(int(k_max), p)
+    if cap < 1:
+        raise ValueError(f"iteration budget must allow k >= 1, got k_max={k_max}")
+    eng = SyncEngine(coarse, fine, p)
+    eng.init(u0)
+    esz = 8 if fine.dtype == torch.float64 else 4
+    if record_iterates is None:
+        record_iterates = (cap + 1) * (p + 1) * fine.dim * esz <= RECORD_LIMIT_BYTES
+    iterates = [BlockVector(eng.lam_a.clone(), check_finite=False)]
+    deltas: list[float] = []
+    slice_deltas: list = []
+    stop_reason = STOP_KMAX
+    k = 0
+    while k < cap:
+        k += 1
+        nxt = eng.lam_b if eng.prev is eng.lam_a else eng.lam_a
+        if record_iterates:
+            nxt.copy_(eng.prev)
+        eng.sweep(k, nxt)
+        delta = eng.read_delta()
+        deltas.append(delta)
+        slice_deltas.append(eng.deltas.to("cpu").numpy().copy())
+        if record_iterates:
+            iterates.append(BlockVector(nxt.clone(), check_finite=False))
+        if delta < epsilon:
+            stop_reason = STOP_THRESHOLD
+            break
+        if k == p:
+            stop_reason = STOP_EXACT
+            break
+        if k == cap:
+            stop_reason = STOP_KMAX
+            break
+    final = BlockVector(eng.prev.clone(), check_finite=False)
+    if not record_iterates:
+        iterates.append(final)
+    return SyncTrace(iterates=iterates, k_final=k, stop_reason=stop_reason, deltas=deltas, final=final,
+                     slice_deltas=slice_deltas)
