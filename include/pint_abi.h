@@ -187,6 +187,17 @@ int pint_sync_sweep(pint_op *coarse, const void *prev, void *next,
 int pint_equal_flag(pint_ctx *ctx, int32_t dtype, int64_t dim, const void *a,
                     const void *b, uint8_t *equal_dev, void *stream);
 
+/*
+ * Chain-input variant for a time-slice shard (multi-GPU): next[k-1] and
+ * deltas_dev[k-1] are INPUTS holding this sweep's new value of slice k-1 and
+ * its delta (received from the GPU owning slice k-1); the F-only branch of
+ * slice k fires when that delta is 0. Otherwise as pint_sync_sweep.
+ */
+int pint_sync_sweep_chain(pint_op *coarse, const void *prev, void *next,
+                          const void *fv, void *gcache, int64_t k, int64_t p,
+                          double *deltas_dev, int32_t *nonfinite_dev,
+                          void *stream);
+
 /* max over deltas_dev[lo..hi) -> *out_dev (device double), deterministic. */
 int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,
                     int64_t hi, double *out_dev, void *stream);

@@ -225,7 +225,20 @@ int pint_sync_sweep(pint_op *coarse, const void *prev, void *next, const void *f
     if (prev == next) pint_throw(PINT_EARG, "prev and next must be distinct iterates");
     if (!is_tri1d(coarse)) pint_throw(PINT_EUNSUPPORTED, "fused sweep is implemented for 1-D implicit coarse operators");
     tri1d_sweep(coarse, (const double *)prev, (double *)next, (const double *)fv, (double *)gcache, k, p,
-                deltas_dev, nonfinite_dev, (cudaStream_t)stream);
+                deltas_dev, nonfinite_dev, (cudaStream_t)stream, 0);
+  });
+}
+
+int pint_sync_sweep_chain(pint_op *coarse, const void *prev, void *next, const void *fv, void *gcache, int64_t k,
+                          int64_t p, double *deltas_dev, int32_t *nonfinite_dev, void *stream) {
+  if (!coarse) return PINT_EARG;
+  return guarded(coarse->ctx, [&] {
+    if (k < 1 || k > p) pint_throw(PINT_EARG, "sweep index must satisfy 1 <= k <= p");
+    if (!prev || !next || !fv || !gcache || !deltas_dev || !nonfinite_dev) pint_throw(PINT_EARG, "null pointer");
+    if (prev == next) pint_throw(PINT_EARG, "prev and next must be distinct iterates");
+    if (!is_tri1d(coarse)) pint_throw(PINT_EUNSUPPORTED, "fused sweep is implemented for 1-D implicit coarse operators");
+    tri1d_sweep(coarse, (const double *)prev, (double *)next, (const double *)fv, (double *)gcache, k, p,
+                deltas_dev, nonfinite_dev, (cudaStream_t)stream, 1);
   });
 }
 

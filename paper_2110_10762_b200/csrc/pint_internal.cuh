@@ -87,6 +87,7 @@ struct pint_op {
   double *d_table = nullptr;
   int batch_cluster = 1;
   int sweep_cluster = 1;
+  int batch_minb = 2;  // CTAs per SM the fine kernel is register-budgeted for (1 or 2)
   // n-D
   int64_t nx = 1, ny = 1, nz = 1;
   void *cg_work = nullptr;   // CG scratch
@@ -104,7 +105,7 @@ void tri1d_coarse_init(pint_op *op, double *lam, int64_t p, double *gcache,
                        cudaStream_t s);
 void tri1d_sweep(pint_op *op, const double *prev, double *next, const double *fv,
                  double *gcache, int64_t k, int64_t p, double *deltas,
-                 int32_t *nonfinite, cudaStream_t s);
+                 int32_t *nonfinite, cudaStream_t s, int chain);
 void tri1d_destroy(pint_op *op);
 
 // n-D launchers (stencil.cu / cg.cu)

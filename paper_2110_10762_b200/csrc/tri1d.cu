@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -368,7 +369,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n}"
       :: "r"(bar), "r"(parity) : "memory");
 }
@@ -399,15 +400,24 @@ __device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t s
 
 #define TAB(f) lds(c.tab + (uint32_t)(f) * 8u)
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // One implicit step on the register-resident chunk. `extra_in` (warp-uniform)
 // is published through the gather and its max over all warps of the slice is
 // returned in *extra_out when WITH_EXTRA. Backward Euler: IN_RAW means the
 // chunk slots hold the raw state (else the pivot-scaled one), OUT_RAW asks for
 // a raw result (else scaled for the next step). The separator is always raw.
-template <int CH, int J, bool CN, bool TAIL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
+template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
 __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
                                          uint32_t sc, double extra_in, double *extra_out) {
-  const bool regular = !TAIL || c.t < P.tb;
+  const bool regular = !GENERAL || c.t < P.tb;
   double xo[CN ? CH : 1];
   if (CN) {
 #pragma unroll
@@ -416,7 +426,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     if (regular) chunk_scale<CH>(x, P.reg);
     else chunk_scale<CH>(x, P.tail);
   }
-  if (P.has_forcing) {
+  if (GENERAL && P.has_forcing) {
     if (c.t == 0) x[0] += P.f_first;
     if (c.t == P.t_last) {
 #pragma unroll
@@ -525,20 +535,20 @@ __device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *s
 // S implicit steps from a raw state to a raw state; the step counter `sc`
 // drives the double-buffered exchange. With extra_out != nullptr the first
 // step also reduces extra_in (max) over the slice.
-template <int CH, int J, bool CN, bool TAIL>
+template <int CH, int J, bool CN, bool GENERAL>
 __device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
                                           uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
   if (S == 1) {
-    if (extra_out) tri_step<CH, J, CN, TAIL, true, true, true>(x, P, c, sc, extra_in, extra_out);
-    else tri_step<CH, J, CN, TAIL, true, true, false>(x, P, c, sc, 0.0, nullptr);
+    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, sc, extra_in, extra_out);
+    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, sc, 0.0, nullptr);
     ++sc;
     return;
   }
-  if (extra_out) tri_step<CH, J, CN, TAIL, true, false, true>(x, P, c, sc, extra_in, extra_out);
-  else tri_step<CH, J, CN, TAIL, true, false, false>(x, P, c, sc, 0.0, nullptr);
+  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, sc, extra_in, extra_out);
+  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, sc, 0.0, nullptr);
   ++sc;
-  for (int64_t s = 1; s < S - 1; ++s, ++sc) tri_step<CH, J, CN, TAIL, false, false, false>(x, P, c, sc, 0.0, nullptr);
-  tri_step<CH, J, CN, TAIL, false, true, false>(x, P, c, sc, 0.0, nullptr);
+  for (int64_t s = 1; s < S - 1; ++s, ++sc) tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, sc, 0.0, nullptr);
+  tri_step<CH, J, CN, GENERAL, false, true, false>(x, P, c, sc, 0.0, nullptr);
   ++sc;
 }
 
@@ -573,8 +583,8 @@ __device__ __forceinline__ void store_chunk(const double (&x)[CH], double *dst, 
   }
 }
 
-template <int CH, int J, bool CN, bool TAIL>
-__global__ void __launch_bounds__(256, 2)
+template <int CH, int J, bool CN, bool GENERAL, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 tri1d_batch_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__restrict__ in,
                    double *__restrict__ out, int64_t stride) {
   extern __shared__ double smem[];
@@ -585,13 +595,13 @@ tri1d_batch_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   double x[CH];
   load_chunk<CH>(x, in + slice * stride, P.N, c.t);
   uint32_t sc = 0;
-  run_steps<CH, J, CN, TAIL>(x, P, c, sc, P.steps, 0.0, nullptr);
+  run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, 0.0, nullptr);
   store_chunk<CH>(x, out + slice * stride, P.N, c.t);
   cluster.sync();
 }
 
 // coarse_init: lam[i] = G(lam[i-1]), i = 1..p (parareal.py:54-63)
-template <int CH, int J, bool CN, bool TAIL>
+template <int CH, int J, bool CN, bool GENERAL>
 __global__ void __launch_bounds__(256, 1)
 tri1d_init_kernel(const __grid_constant__ Tri1DParams<CH> P, double *lam, double *gcache, int64_t p) {
   extern __shared__ double smem[];
@@ -602,7 +612,7 @@ tri1d_init_kernel(const __grid_constant__ Tri1DParams<CH> P, double *lam, double
   load_chunk<CH>(x, lam, P.N, c.t);
   uint32_t sc = 0;
   for (int64_t i = 1; i <= p; ++i) {
-    run_steps<CH, J, CN, TAIL>(x, P, c, sc, P.steps, 0.0, nullptr);
+    run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, 0.0, nullptr);
     store_chunk<CH>(x, lam + i * P.N, P.N, c.t);
     if (gcache) store_chunk<CH>(x, gcache + i * P.N, P.N, c.t);
   }
@@ -617,42 +627,70 @@ __device__ __forceinline__ double warp_max(double v) {
 
 // One synchronous sweep with the coarse chain fused with the correction
 // (parareal.py:119-127): the running iterate next[i-1] never leaves the SMs.
-template <int CH, int J, bool CN, bool TAIL>
+template <int CH, int J, bool CN, bool GENERAL>
 __global__ void __launch_bounds__(256, 1)
 tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__restrict__ prev,
                    double *__restrict__ next, const double *__restrict__ fv, double *__restrict__ gcache,
-                   int64_t k, int64_t p, double *deltas, int32_t *nonfinite) {
+                   int64_t k, int64_t p, double *deltas, int32_t *nonfinite, int chain_in) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   StepCtx c = setup_ctx<CH, J>(P, smem, rank);
   const int64_t N = P.N;
   double x[CH];
-  load_chunk<CH>(x, prev + (k - 1) * N, N, c.t);
-  if (next != prev) store_chunk<CH>(x, next + (k - 1) * N, N, c.t);
-  if (rank == 0 && threadIdx.x == 0) deltas[k - 1] = 0.0;
+  // chain_in: next[k-1] / deltas[k-1] already hold this sweep's value of slice
+  // k-1 (received from the previous GPU of the chain); else slice k-1 is the
+  // frozen prefix (next[k-1] = prev[k-1], delta 0).
+  const double delta_in = chain_in ? deltas[k - 1] : 0.0;
+  if (chain_in) {
+    load_chunk<CH>(x, next + (k - 1) * N, N, c.t);
+  } else {
+    load_chunk<CH>(x, prev + (k - 1) * N, N, c.t);
+    store_chunk<CH>(x, next + (k - 1) * N, N, c.t);
+  }
+  __syncthreads();
+  if (!chain_in && rank == 0 && threadIdx.x == 0) deltas[k - 1] = 0.0;
   uint32_t sc = 0;
   double dpart = 0.0;  // warp-uniform partial max of the previous slice
   bool bad = false;
   const int64_t base = (int64_t)c.t * CH;
+  // this thread's private staging row for F(old), G(old), prev of the slice
+  // being corrected: filled by cp.async while the coarse step runs
+  const uint32_t row = smem_u32(smem + (15 + 4 * J) * c.TB + 8 * (c.nW + 1) + 2) +
+                       (uint32_t)threadIdx.x * (uint32_t)(3 * CH + 2) * 8u;
+  const int64_t rem_ = N - base;
+  const int nvalid = rem_ <= 0 ? 0 : (rem_ >= CH ? CH : (int)rem_);
+  const bool vec16 = ((N & 1) == 0) && nvalid == CH;
   for (int64_t i = k; i <= p; ++i) {
+    {
+      const double *srcs[3] = {fv + i * N + base, gcache + i * N + base, prev + i * N + base};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const uint32_t dst = row + (uint32_t)(a * CH) * 8u;
+        if (vec16) {
+#pragma unroll
+          for (int j = 0; j < CH; j += 2) cp_async16(dst + j * 8u, srcs[a] + j);
+        } else {
+          for (int j = 0; j < nvalid; ++j) cp_async8(dst + j * 8u, srcs[a] + j);
+        }
+      }
+      cp_async_commit();
+    }
     double dprev = 0.0;
-    run_steps<CH, J, CN, TAIL>(x, P, c, sc, P.steps, dpart, &dprev);
+    run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, dpart, &dprev);
     if (i > k && rank == 0 && threadIdx.x == 0) deltas[i - 1] = dprev;
-    const bool fonly = (i == k) || (dprev == 0.0);
-    const double *f = fv + i * N + base;
-    const double *go = gcache + i * N + base;
-    const double *pv = prev + i * N + base;
+    const bool fonly = (i == k) ? (delta_in == 0.0) : (dprev == 0.0);
     double *gw = gcache + i * N + base;
     double *nw = next + i * N + base;
+    cp_async_wait_all();
     double dm = 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       if (base + j < N) {
         const double g = x[j];
-        const double fj = f[j];
-        const double v = fonly ? fj : (g + fj) - go[j];
-        dm = fmax(dm, fabs(v - pv[j]));
+        const double fj = lds(row + (uint32_t)j * 8u);
+        const double v = fonly ? fj : (g + fj) - lds(row + (uint32_t)(CH + j) * 8u);
+        dm = fmax(dm, fabs(v - lds(row + (uint32_t)(2 * CH + j) * 8u)));
         bad |= !isfinite(v);
         gw[j] = g;
         nw[j] = v;
@@ -737,25 +775,29 @@ static size_t smem_bytes(const Tri1DPlan &pl, int TB) {
 
 enum class TriKind { Batch, Init, Sweep };
 
-template <int CH, int J, bool CN, bool TAIL>
+template <int CH, int J, bool CN, bool GENERAL>
 static void run_kernel(TriKind kind, const pint_op *op, int grid_slices, int cl, cudaStream_t s,
                        const double *in, double *out, int64_t stride, double *lam, double *gcache,
                        int64_t p, const double *prev, double *next, const double *fv, int64_t k,
-                       double *deltas, int32_t *nonfinite) {
+                       double *deltas, int32_t *nonfinite, int chain) {
   const Tri1DPlan &pl = op->plan;
   Tri1DParams<CH> P = make_params<CH>(op);
   const int TB = pl.T / cl;
   const size_t sm = smem_bytes(pl, TB);
   switch (kind) {
     case TriKind::Batch:
-      launch_cluster(tri1d_batch_kernel<CH, J, CN, TAIL>, grid_slices * cl, TB, cl, sm, s, P, in, out, stride);
+      if (op->batch_minb == 1)
+        launch_cluster(tri1d_batch_kernel<CH, J, CN, GENERAL, 1>, grid_slices * cl, TB, cl, sm, s, P, in, out, stride);
+      else
+        launch_cluster(tri1d_batch_kernel<CH, J, CN, GENERAL, 2>, grid_slices * cl, TB, cl, sm, s, P, in, out, stride);
       break;
     case TriKind::Init:
-      launch_cluster(tri1d_init_kernel<CH, J, CN, TAIL>, cl, TB, cl, sm, s, P, lam, gcache, p);
+      launch_cluster(tri1d_init_kernel<CH, J, CN, GENERAL>, cl, TB, cl, sm, s, P, lam, gcache, p);
       break;
     case TriKind::Sweep:
-      launch_cluster(tri1d_sweep_kernel<CH, J, CN, TAIL>, cl, TB, cl, sm, s, P, prev, next, fv, gcache, k, p,
-                     deltas, nonfinite);
+      launch_cluster(tri1d_sweep_kernel<CH, J, CN, GENERAL>, cl, TB, cl,
+                     sm + sizeof(double) * (size_t)TB * (3 * CH + 2), s, P, prev, next, fv, gcache, k, p,
+                     deltas, nonfinite, chain);
       break;
   }
 }
@@ -764,32 +806,33 @@ template <int CH, int J, bool CN>
 static void run_kernel_t(TriKind kind, const pint_op *op, int grid_slices, int cl, cudaStream_t s,
                          const double *in, double *out, int64_t stride, double *lam, double *gcache,
                          int64_t p, const double *prev, double *next, const double *fv, int64_t k,
-                         double *deltas, int32_t *nonfinite) {
-  if (op->plan.tb < op->plan.T)
+                         double *deltas, int32_t *nonfinite, int chain) {
+  // GENERAL: a partially filled (tail) thread or boundary forcing; the fast path has neither
+  if (op->plan.tb < op->plan.T || op->plan.f_first != 0.0 || op->plan.f_last != 0.0)
     run_kernel<CH, J, CN, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
-                                deltas, nonfinite);
+                                deltas, nonfinite, chain);
   else
     run_kernel<CH, J, CN, false>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
-                                 deltas, nonfinite);
+                                 deltas, nonfinite, chain);
 }
 
 template <int CH, bool CN>
 static void run_kernel_j(TriKind kind, const pint_op *op, int grid_slices, int cl, cudaStream_t s,
                          const double *in, double *out, int64_t stride, double *lam, double *gcache,
                          int64_t p, const double *prev, double *next, const double *fv, int64_t k,
-                         double *deltas, int32_t *nonfinite) {
+                         double *deltas, int32_t *nonfinite, int chain) {
   switch (op->plan.J) {
     case 1:
       run_kernel_t<CH, 1, CN>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
-                            deltas, nonfinite);
+                            deltas, nonfinite, chain);
       break;
     case 2:
       run_kernel_t<CH, 2, CN>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
-                            deltas, nonfinite);
+                            deltas, nonfinite, chain);
       break;
     default:
       run_kernel_t<CH, 4, CN>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
-                            deltas, nonfinite);
+                            deltas, nonfinite, chain);
       break;
   }
 }
@@ -797,9 +840,9 @@ static void run_kernel_j(TriKind kind, const pint_op *op, int grid_slices, int c
 static void run_any(TriKind kind, const pint_op *op, int grid_slices, int cl, cudaStream_t s,
                     const double *in, double *out, int64_t stride, double *lam, double *gcache, int64_t p,
                     const double *prev, double *next, const double *fv, int64_t k, double *deltas,
-                    int32_t *nonfinite) {
-  if (op->plan.cn) run_kernel_j<16, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite);
-  else run_kernel_j<32, false>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite);
+                    int32_t *nonfinite, int chain = 0) {
+  if (op->plan.cn) run_kernel_j<16, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite, chain);
+  else run_kernel_j<32, false>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite, chain);
 }
 
 void tri1d_setup(pint_op *op) {
@@ -827,6 +870,11 @@ void tri1d_setup(pint_op *op) {
   // CTA split of the T threads of a slice (does not change the arithmetic)
   op->batch_cluster = std::max(1, pl.T / 256);
   op->sweep_cluster = std::min(16, std::max(1, pl.T / 128));
+  if (const char *mb = getenv("PINT_TRI_MINB")) op->batch_minb = atoi(mb) == 1 ? 1 : 2;
+  if (const char *bc = getenv("PINT_TRI_BATCH_CL")) {
+    const int v = atoi(bc);
+    if (v >= 1 && v <= 16 && pl.T % v == 0 && (pl.T / v) % 32 == 0 && pl.T / v <= 256) op->batch_cluster = v;
+  }
 }
 
 void tri1d_destroy(pint_op *op) {
@@ -851,9 +899,9 @@ void tri1d_coarse_init(pint_op *op, double *lam, int64_t p, double *gcache, cuda
 }
 
 void tri1d_sweep(pint_op *op, const double *prev, double *next, const double *fv, double *gcache, int64_t k,
-                 int64_t p, double *deltas, int32_t *nonfinite, cudaStream_t s) {
+                 int64_t p, double *deltas, int32_t *nonfinite, cudaStream_t s, int chain) {
   run_any(TriKind::Sweep, op, 1, op->sweep_cluster, s, nullptr, nullptr, 0, nullptr, gcache, p, prev, next, fv,
-          k, deltas, nonfinite);
+          k, deltas, nonfinite, chain);
 }
 
 // Host-only plan export (include/pint_abi.h: pint_tri1d_plan_host).

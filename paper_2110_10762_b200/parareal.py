@@ -191,35 +191,55 @@ class SyncEngine:
         self.prev = self.lam_a
         self.flag.zero_()
 
-    def sweep(self, k: int, nxt: torch.Tensor) -> None:
-        """Sweep k (device work only, stream-ordered): nxt <- new iterate."""
+    def fine_batch(self, k: int, fine_done_event=None) -> None:
+        """fv[i] = F(prev[i-1]) for i in [k, p]: one launch over all live slices."""
         p, n = self.p, self.fine.dim
-        prev = self.prev
-        self.fine.apply_ptr(prev[k - 1].data_ptr(), self.fv[k].data_ptr(), p - k + 1, n)
+        self.fine.apply_ptr(self.prev[k - 1].data_ptr(), self.fv[k].data_ptr(), p - k + 1, n)
+        if fine_done_event is not None:
+            fine_done_event.record(torch.cuda.current_stream(self.fine.device))
+
+    def coarse_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
+        """Fused G chain + correction + per-slice delta for slices [k, p].
+        chain_in: nxt[k-1] and deltas[k-1] already hold this sweep's slice k-1."""
+        p, prev = self.p, self.prev
         if self.fused:
-            rc = self.lib.pint_sync_sweep(
-                self.coarse.handle, ctypes.c_void_p(prev.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
-                ctypes.c_void_p(self.fv.data_ptr()), ctypes.c_void_p(self.gcache.data_ptr()), int(k), int(p),
-                ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()),
-                _stream(self.coarse))
+            fn = self.lib.pint_sync_sweep_chain if chain_in else self.lib.pint_sync_sweep
+            rc = fn(self.coarse.handle, ctypes.c_void_p(prev.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
+                    ctypes.c_void_p(self.fv.data_ptr()), ctypes.c_void_p(self.gcache.data_ptr()), int(k), int(p),
+                    ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()),
+                    _stream(self.coarse))
             _native.check(rc, _ctx(self.coarse), "pint_sync_sweep")
         else:
-            self._generic_sweep(k, nxt)
-        rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, p + 1,
+            self._generic_sweep(k, nxt, chain_in)
+
+    def reduce_delta(self, k: int) -> None:
+        rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, self.p + 1,
                                       ctypes.c_void_p(self.dmax.data_ptr()), _stream(self.fine))
         _native.check(rc, _ctx(self.fine), "pint_max_reduce")
+
+    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None) -> None:
+        """Sweep k (device work only, stream-ordered): nxt <- new iterate."""
+        self.fine_batch(k, fine_done_event)
+        self.coarse_sweep(k, nxt)
+        self.reduce_delta(k)
         self.prev = nxt
 
-    def _generic_sweep(self, k: int, nxt: torch.Tensor) -> None:
+    def launches_per_sweep(self) -> int:
+        """Our kernel launches per sweep (fused path: F batch, coarse sweep,
+        max-reduce)."""
+        return 3 if self.fused else 1 + 3 * self.p
+
+    def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
         """Coarse chain + correction for coarse operators without a fused
         sweep kernel (CG coarse in 2-D/3-D): same values, one launch per slice."""
         p, prev = self.p, self.prev
-        nxt[k - 1].copy_(prev[k - 1])
-        self.deltas[k - 1] = 0.0
+        if not chain_in:
+            nxt[k - 1].copy_(prev[k - 1])
+            self.deltas[k - 1] = 0.0
         g = torch.empty(1, self.fine.dim, dtype=self.fine.dtype, device=nxt.device)
         for i in range(k, p + 1):
             self.coarse.apply_ptr(nxt[i - 1].data_ptr(), g.data_ptr(), 1, self.fine.dim)
-            f_only = (i == k) or float(self.deltas[i - 1]) == 0.0
+            f_only = float(self.deltas[i - 1]) == 0.0 if (chain_in or i > k) else True
             self.fonly.fill_(1 if f_only else 0)
             correct_into(self.fine, g, self.fv[i:i + 1], self.gcache[i:i + 1], prev[i:i + 1], nxt[i:i + 1],
                          self.fonly, self.deltas[i:i + 1], self.flag, 1)

@@ -1,0 +1,97 @@
+"""Asynchronous Parareal on the GPU: the reference's deterministic event
+semantics (same seeds -> same activations, reads and values), exactness
+cascade, and the zero-delay reduction to the synchronous sweep."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ("rf_s5_d1_p6", "rf_s9_d2_p6", "adv_s3_d2_p5", "rr_s0_d0_p6_eps", "rf_s4_d3_p7_eps")
+
+
+def heat_pair(gpu, n):
+    ivp = gpu.heat1d_system(n, 1.0, 23.0, 23.0, 30.0, 0.2)
+    return ivp, gpu.backward_euler_propagator(ivp, 0.2, 1), gpu.trapezoidal_propagator(ivp, 0.2, 100)
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_async_trace_matches_reference(gpu, tag):
+    g = golden("async_traces.npz")
+    sched = json.loads(str(g[f"{tag}_sched"]))
+    ivp, coarse, fine = heat_pair(gpu, 4)
+    s = gpu.AsyncSchedule(seed=sched["seed"], delay_bound=sched["delay_bound"], policy=sched["policy"])
+    tr = gpu.run_async_parareal(coarse, fine, ivp.u0, sched["p"], s, epsilon=sched["eps"])
+    comps = np.array([e.component for e in tr.events])
+    reads = np.array([[r[2] for r in e.reads] for e in tr.events])
+    assert np.array_equal(comps, g[f"{tag}_components"])
+    assert np.array_equal(reads, g[f"{tag}_reads"])
+    assert tr.stop_reason == str(g[f"{tag}_stop"])
+    assert np.array_equal(tr.per_component_counts, g[f"{tag}_counts"])
+    final = tr.state_after(len(tr.events) - 1).data
+    assert np.max(np.abs(final - g[f"{tag}_final"]) / np.abs(g[f"{tag}_final"])) < 1e-12
+
+
+def test_event_replay_and_remembered_slot(gpu):
+    ivp, coarse, fine = heat_pair(gpu, 4)
+    tr = gpu.run_async_parareal(coarse, fine, ivp.u0, 5, gpu.AsyncSchedule(seed=12, delay_bound=2))
+    prev_fresh = {}
+    for idx, ev in enumerate(tr.events):
+        reads = {slot: (src, v) for src, slot, v in ev.reads}
+        if ev.component in prev_fresh:
+            assert reads[gpu.REMEMBERED_SLOT] == prev_fresh[ev.component]
+        else:
+            assert reads[gpu.REMEMBERED_SLOT][1] == 0
+        prev_fresh[ev.component] = reads[gpu.FRESH_SLOT]
+        vals = {slot: tr.version_value(src, v) for src, slot, v in ev.reads}
+        want = gpu.parareal_update(coarse, fine, vals[gpu.FRESH_SLOT], vals[gpu.REMEMBERED_SLOT])
+        assert np.array_equal(want, tr.snapshots[idx][ev.component]), idx
+    assert gpu.validate_schedule(tr).ok
+
+
+def test_quiescence_is_the_sequential_fine_solution_bitwise(gpu):
+    ivp, coarse, fine = heat_pair(gpu, 4)
+    p = 6
+    seq = gpu.sequential_fine_solve(fine, ivp.u0, p).data
+    for seed, d in [(5, 1), (9, 2), (14, 3)]:
+        tr = gpu.run_async_parareal(coarse, fine, ivp.u0, p, gpu.AsyncSchedule(seed=seed, delay_bound=d))
+        assert tr.stop_reason == "quiescence"
+        assert np.array_equal(tr.state_after(len(tr.events) - 1).data, seq)
+
+
+def test_zero_delay_round_robin_is_the_sync_sweep_bitwise(gpu):
+    ivp = gpu.scalar_decay_system(rate=1.0, t_final=8.0)
+    p = 8
+    coarse = gpu.backward_euler_propagator(ivp, 1.0, 1)
+    fine = gpu.trapezoidal_propagator(ivp, 1.0, 25)
+    sync = gpu.run_parareal(coarse, fine, ivp.u0, p, 1e-5)
+    assert sync.stop_reason == "threshold" and sync.k_final == 7
+    sched = gpu.AsyncSchedule(seed=0, delay_bound=0, policy=gpu.POLICY_ROUND_ROBIN)
+    tr = gpu.run_async_parareal(coarse, fine, ivp.u0, p, sched, epsilon=1e-5)
+    assert tr.stop_reason == "stop-predicate"
+    _, kappa = gpu.update_counts(tr)
+    assert kappa == sync.k_final
+    for cycle in range(sync.k_final):
+        assert np.array_equal(tr.state_after(cycle * p + p - 1).data, sync.iterates[cycle + 1].data), cycle
+
+
+def test_c1_async_reaches_the_sync_solution(gpu):
+    """Async-Parareal must reach the same converged solution within the
+    stopping tolerance (north star)."""
+    from oracle import heat_oracle as H
+    n, p = 1024, 16
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 100)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    tr = gpu.run_async_parareal(coarse, fine, u0, p, gpu.AsyncSchedule(seed=3, delay_bound=2), epsilon=1e-10,
+                                record_snapshots=False)
+    final = tr.state_after(len(tr.events) - 1).data
+    assert np.max(np.abs(final - seq)) < 1e-8
+    _, kappa = gpu.update_counts(tr)
+    sync = gpu.run_parareal(coarse, fine, u0, p, 1e-10)
+    assert kappa >= sync.k_final
