@@ -198,6 +198,22 @@ int pint_sync_sweep_chain(pint_op *coarse, const void *prev, void *next,
                           double *deltas_dev, int32_t *nonfinite_dev,
                           void *stream);
 
+/*
+ * Asynchronous Parareal with real concurrency on one GPU (persistent launch;
+ * see tri1d.cu). lam0 = coarse initial iterate ((p+1) x dim, device). Stops
+ * when every slice has consumed the newest predecessor version and every last
+ * change is < epsilon; epsilon < 0 runs to exact quiescence. delay_frac > 0
+ * injects a seeded per-activation delay U(0, delay_frac) * t_F. Writes the
+ * newest published iterate to final_out (device), activations per slice to
+ * counts_out (host, p+1), and info_out (host, 5) = {activations, stop code
+ * (1 converged / 2 max_events), non-finite, seqlock retries, clusters}.
+ * Synchronous with respect to the host.
+ */
+int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p,
+                   double epsilon, int64_t max_events, double delay_frac,
+                   uint64_t seed, void *final_out, int64_t *counts_out,
+                   int64_t *info_out, void *stream);
+
 /* max over deltas_dev[lo..hi) -> *out_dev (device double), deterministic. */
 int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,
                     int64_t hi, double *out_dev, void *stream);

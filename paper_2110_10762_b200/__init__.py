@@ -26,6 +26,8 @@ from .async_parareal import (
     async_stop_check,
     run_async_parareal,
     simulate_parareal_async,
+    run_async_parareal_device,
+    DeviceAsyncResult,
 )
 from .errors import (
     ConfigError,

@@ -176,3 +176,62 @@ def run_async_parareal(coarse, fine, u0, p: int, schedule: AsyncSchedule, epsilo
             return async_stop_check(view.last_deltas[1:], eps, view.drained)
 
     return simulate_parareal_async(coarse, fine, init, schedule, stop=stop, record_snapshots=record_snapshots)
+
+
+class DeviceAsyncResult:
+    """Outcome of ``run_async_parareal_device``."""
+
+    def __init__(self, final, counts, info, wall_s):
+        self.final = final
+        self.per_component_counts = counts
+        self.activations = int(info[0])
+        self.stop_reason = {1: "converged", 2: "max_events"}.get(int(info[1]), "unknown")
+        self.retries = int(info[3])
+        self.concurrent_clusters = int(info[4])
+        self.wall_s = wall_s
+
+    @property
+    def kappa(self) -> int:
+        """Busiest worker's activation count (the paper's kappa(k~))."""
+        return int(np.max(self.per_component_counts[1:])) if len(self.per_component_counts) > 1 else 0
+
+
+def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = None, *,
+                              max_events: int = 200_000, delay_frac: float = 0.0,
+                              seed: int = 0) -> DeviceAsyncResult:
+    """Asynchronous Parareal with real concurrency on the GPU (PAPER.md
+    Algorithm 2): one persistent launch; thread-block clusters act as workers
+    that claim slice activations, read the freshest published predecessor
+    (no waiting, versioned ring buffers) and publish their update. Stops when
+    every slice is drained and its last change is below epsilon, or at exact
+    quiescence when epsilon is None."""
+    import time
+
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+    if epsilon is not None and epsilon <= 0.0:
+        raise ValueError(f"epsilon must be positive, got {epsilon}")
+    from .model import with_register_layout
+    coarse = with_register_layout(coarse, fine.info.points_per_thread) if fine.is_tridiagonal else coarse
+    lam = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")
+    lam[0] = _u0_tensor(coarse, u0)
+    _coarse_init_into(coarse, lam, p, None)
+    out = torch.empty_like(lam)
+    counts = np.zeros(p + 1, dtype=np.int64)
+    info = np.zeros(5, dtype=np.int64)
+    lib = _native.load_library()
+    torch.cuda.synchronize(fine.device)
+    t0 = time.perf_counter()
+    rc = lib.pint_async_run(fine.handle, coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
+                            float(-1.0 if epsilon is None else epsilon), int(max_events), float(delay_frac),
+                            int(seed), ctypes.c_void_p(out.data_ptr()), counts.ctypes.data_as(ctypes.c_void_p),
+                            info.ctypes.data_as(ctypes.c_void_p),
+                            ctypes.c_void_p(_device.stream_ptr(fine.device)))
+    _native.check(rc, fine._ctx.handle, "pint_async_run")
+    wall = time.perf_counter() - t0
+    if info[2]:
+        raise ValueError("block entries must be finite")
+    res = DeviceAsyncResult(BlockVector(out, check_finite=False), counts, info, wall)
+    if res.stop_reason == "max_events":
+        raise HorizonExhausted(f"no stop condition met within {max_events} activations", res)
+    return res

@@ -842,6 +842,7 @@ static void run_any(TriKind kind, const pint_op *op, int grid_slices, int cl, cu
                     const double *prev, double *next, const double *fv, int64_t k, double *deltas,
                     int32_t *nonfinite, int chain = 0) {
   if (op->plan.cn) run_kernel_j<16, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite, chain);
+  else if (op->plan.CH == 16) run_kernel_j<16, false>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite, chain);
   else run_kernel_j<32, false>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k, deltas, nonfinite, chain);
 }
 
@@ -851,8 +852,13 @@ void tri1d_setup(pint_op *op) {
   const bool cn = d.rule == PINT_RULE_TRAPEZOIDAL;
   // backward Euler keeps 32 points per thread in registers; the trapezoidal
   // rule also keeps the previous state (x+ = 2 K^{-1}(x + dt/2 c) - x), so 16
-  const int CH = cn ? 16 : 32;
-  if (d.layout_ch && d.layout_ch != CH) pint_throw(PINT_EARG, "layout_ch must be 32 (backward Euler) or 16 (trapezoidal)");
+  // (layout_ch = 16 is also accepted for backward Euler, so that a coarse
+  //  operator can share the register layout of a trapezoidal fine operator)
+  int CH = cn ? 16 : 32;
+  if (d.layout_ch) {
+    if (d.layout_ch == 16 || (d.layout_ch == 32 && !cn)) CH = d.layout_ch;
+    else pint_throw(PINT_EARG, "layout_ch must be 32 or 16 (backward Euler) or 16 (trapezoidal)");
+  }
   if (d.dtype != PINT_F64) pint_throw(PINT_EUNSUPPORTED, "1-D implicit propagators compute in float64");
   // coefficients formed like the reference's dense matrices:
   // eye - dt * a_mat (BE), half = 0.5 * dt * a_mat (trapezoidal)
@@ -943,6 +949,403 @@ extern "C" int pint_tri1d_plan_host(const pint_op_desc *d, int32_t *dims_out, do
     }
     return PINT_OK;
   } catch (const PintError &e) {
+    return e.code;
+  }
+}
+
+// ======================================================= asynchronous runtime
+//
+// Asynchronous Parareal with real concurrency (reference semantics:
+// async_parareal.py:24-84, Algorithm 2): one persistent launch whose
+// thread-block clusters repeatedly claim a slice activation from an atomic
+// ticket queue (round-robin order, per-slice try-lock), run
+//     F(remembered) -> read the freshest published predecessor -> G(fresh)
+//     -> new = F-only ? F(rem) : (G(fresh) + F(rem)) - G(rem) -> publish
+// and never wait on another cluster: predecessor states are read from a
+// ring of R version-stamped buffers with a seqlock check (retry if the
+// writer lapped the slot), so no co-residency is required and staleness is
+// whatever the hardware schedule produces. G(rem) is the previous
+// activation's G(fresh) (cached per slice). Termination (checked by the
+// cluster that just published): every slice drained (consumed the newest
+// predecessor version) and every last change < eps, or, with eps < 0, exact
+// quiescence (every slice's last activation was F-only on the newest
+// predecessor version).
+
+struct AsyncArgs {
+  double *ring;            // (P+1) x R x N  published versions
+  double *remb;            // (P+1) x N      remembered predecessor reading
+  double *gremb;           // (P+1) x N      G(remembered)
+  double *scratch;         // nclusters x 2 x N (F result, fresh reading)
+  long long *ver;          // (P+1) newest published version per slice
+  long long *vrem;         // (P+1) version of the remembered reading
+  long long *consumed;     // (P+1) predecessor version consumed at the last activation
+  int *busy;               // (P+1) try-lock
+  int *stable;             // (P+1) last activation was F-only
+  long long *counts;       // (P+1) activations per slice
+  double *last_delta;      // (P+1)
+  unsigned long long *ticket;
+  int *stop;               // 1 = converged, 2 = max_events reached
+  int *nonfinite;
+  long long *events;
+  long long *retries;
+  int64_t P, N;
+  int R;
+  double eps;              // < 0: exact quiescence
+  int64_t max_events;
+  double delay_frac;       // injected delay per activation: U(0, delay_frac) * t_F
+  unsigned long long seed;
+};
+
+__device__ __forceinline__ long long ld_acquire_s64(const long long *p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s64(long long *p, long long v) {
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Stop test (async_parareal.py:52-58 / quiescence): every slice drained and
+// every last change < eps (eps >= 0), or every slice stable (eps < 0).
+__device__ bool async_done(const AsyncArgs &A) {
+  for (long long s = 1; s <= A.P; ++s) {
+    const long long vp = (s - 1 == 0) ? 0 : ld_acquire_s64(A.ver + s - 1);
+    if (*(volatile long long *)(A.consumed + s) != vp) return false;
+    if (A.eps >= 0.0 ? !(*(volatile double *)(A.last_delta + s) < A.eps) : !*(volatile int *)(A.stable + s))
+      return false;
+  }
+  return true;
+}
+
+template <int CH>
+__device__ __forceinline__ void load_chunk_cg(double (&x)[CH], const double *src, int64_t N, int t) {
+  const int64_t base = (int64_t)t * CH;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) x[j] = (base + j < N) ? __ldcg(src + base + j) : 0.0;
+}
+
+// broadcast a few int64 control words from rank 0 / thread 0 to every CTA
+__device__ __forceinline__ void ctl_broadcast(long long *ctl, int CL, int n) {
+  cg::cluster_group cluster = cg::this_cluster();
+  for (int r = 0; r < CL; ++r) {
+    long long *dst = cluster.map_shared_rank(ctl, r);
+    for (int q = 0; q < n; ++q) dst[q] = ctl[q];
+  }
+}
+
+template <int CH, int J, bool CNF, bool CNG, bool GENERAL>
+__global__ void __launch_bounds__(256, 1)
+tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_constant__ Tri1DParams<CH> PG,
+                   const AsyncArgs A) {
+  extern __shared__ double smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int TB = blockDim.x;
+  const int NF = 15 + 4 * J;
+  const int nW = PF.nW;
+  // layout: [tabF][tabG][gather 8(nW+1)][2 mbarriers][ctl 8 x int64][red 32]
+  double *tabF = smem;
+  double *tabG = smem + NF * TB;
+  double *gbuf = tabG + NF * TB;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 8 * (nW + 1));
+  long long *ctl = reinterpret_cast<long long *>(bars + 2);
+  double *red = reinterpret_cast<double *>(ctl + 8);
+  StepCtx cF, cG;
+  cF.TB = cG.TB = TB;
+  cF.CL = cG.CL = PF.T / TB;
+  cF.nW = cG.nW = nW;
+  cF.t = cG.t = rank * TB + threadIdx.x;
+  cF.lane = cG.lane = threadIdx.x & 31;
+  cF.Wg = cG.Wg = cF.t >> 5;
+  for (int f = 0; f < NF; ++f) {
+    tabF[threadIdx.x * NF + f] = PF.table[(size_t)f * PF.T + cF.t];
+    tabG[threadIdx.x * NF + f] = PG.table[(size_t)f * PG.T + cF.t];
+  }
+  cF.tab = smem_u32(tabF + threadIdx.x * NF);
+  cG.tab = smem_u32(tabG + threadIdx.x * NF);
+  for (int i = threadIdx.x; i < 8 * (nW + 1); i += TB) gbuf[i] = 0.0;
+  cF.gbuf = cG.gbuf = smem_u32(gbuf);
+  cF.mbar = cG.mbar = smem_u32(bars);
+  if (threadIdx.x == 0) {
+    mbar_init(cF.mbar, 1);
+    mbar_init(cF.mbar + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster.sync();
+
+  const int64_t N = A.N, P = A.P;
+  const int CL = cF.CL;
+  const int64_t cid = blockIdx.x / CL;
+  double *sF = A.scratch + (size_t)cid * 2 * N;
+  double *sFresh = sF + N;
+  const int64_t base = (int64_t)cF.t * CH;
+  uint32_t sc = 0;
+  double x[CH];
+  bool bad = false;
+  for (;;) {
+    // ---- claim an activation (rank 0, thread 0), broadcast to the cluster
+    if (rank == 0 && threadIdx.x == 0) {
+      long long slice = -1;
+      unsigned backoff = 32;
+      for (;;) {
+        if (*(volatile int *)A.stop) break;
+        const unsigned long long tk = atomicAdd(A.ticket, 1ull);
+        if (tk >= (unsigned long long)A.max_events * 64ull) {  // livelock guard
+          atomicCAS(A.stop, 0, 2);
+          break;
+        }
+        const long long i = 1 + (long long)(tk % (unsigned long long)P);
+        if (atomicCAS(A.busy + i, 0, 1) != 0) continue;
+        const long long vp = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
+        if (*(volatile int *)(A.stable + i) && *(volatile long long *)(A.consumed + i) == vp) {
+          // nothing new to consume: an activation would reproduce the same
+          // value, i.e. a zero change; record it as such without publishing
+          *(volatile double *)(A.last_delta + i) = 0.0;
+          __threadfence();
+          atomicExch(A.busy + i, 0);
+          if (async_done(A)) atomicExch(A.stop, 1);
+          __nanosleep(backoff);
+          backoff = min(backoff * 2, 4096u);
+          continue;
+        }
+        slice = i;
+        break;
+      }
+      ctl[0] = slice;
+      ctl_broadcast(ctl, CL, 1);
+    }
+    cluster.sync();
+    const long long i = ctl[0];
+    if (i < 0) break;
+
+    // ---- F(remembered)
+    const unsigned long long tf0 = globaltimer();
+    load_chunk_cg<CH>(x, A.remb + i * N, N, cF.t);
+    run_steps<CH, J, CNF, GENERAL>(x, PF, cF, sc, PF.steps, 0.0, nullptr);
+    store_chunk<CH>(x, sF, N, cF.t);
+    if (A.delay_frac > 0.0 && rank == 0 && threadIdx.x == 0) {
+      const unsigned long long tF = globaltimer() - tf0;
+      const unsigned long long h = mix64(A.seed ^ ((unsigned long long)i << 32) ^ (unsigned long long)A.counts[i]);
+      const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
+      const unsigned long long until = globaltimer() + (unsigned long long)(u * A.delay_frac * (double)tF);
+      while (globaltimer() < until) __nanosleep(1000);
+    }
+
+    // ---- freshest predecessor (seqlock read of the ring)
+    long long v = 0;
+    for (int attempt = 0;; ++attempt) {
+      if (rank == 0 && threadIdx.x == 0) {
+        ctl[1] = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
+        ctl_broadcast(ctl + 1, CL, 1);
+      }
+      cluster.sync();
+      v = ctl[1];
+      load_chunk_cg<CH>(x, A.ring + ((size_t)(i - 1) * A.R + (size_t)(v % A.R)) * N, N, cF.t);
+      __syncthreads();
+      if (rank == 0 && threadIdx.x == 0) {
+        const long long v2 = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
+        ctl[2] = (v2 <= v + A.R - 2) ? 1 : 0;
+        if (!ctl[2]) atomicAdd((unsigned long long *)A.retries, 1ull);
+        ctl_broadcast(ctl + 2, CL, 1);
+      }
+      cluster.sync();
+      if (ctl[2]) break;
+    }
+    const long long vr = A.vrem[i];
+    // bitwise comparison with the remembered reading (array_equal semantics)
+    double mism = 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (base + j < N && !(x[j] == __ldcg(A.remb + i * N + base + j))) mism = 1.0;
+    mism = warp_max(mism);
+    store_chunk<CH>(x, sFresh, N, cF.t);
+
+    // ---- G(fresh), with the mismatch flag reduced over the slice on the way
+    double anymism = 0.0;
+    run_steps<CH, J, CNG, GENERAL>(x, PG, cG, sc, PG.steps, mism, &anymism);
+    const bool fonly = (v == vr) || (anymism == 0.0);
+
+    // ---- correction, delta, publish into the next ring slot
+    const long long vi = A.ver[i];
+    const double *cur = A.ring + ((size_t)i * A.R + (size_t)(vi % A.R)) * N + base;
+    double *dst = A.ring + ((size_t)i * A.R + (size_t)((vi + 1) % A.R)) * N + base;
+    double *gw = A.gremb + i * N + base;
+    double *rw = A.remb + i * N + base;
+    double dm = 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      if (base + j < N) {
+        const double g = x[j];
+        const double f = __ldcg(sF + base + j);
+        const double nv = fonly ? f : (g + f) - __ldcg(gw + j);
+        dm = fmax(dm, fabs(nv - __ldcg(cur + j)));
+        bad |= !isfinite(nv);
+        dst[j] = nv;
+        gw[j] = g;
+        rw[j] = __ldcg(sFresh + base + j);
+      }
+    }
+    dm = warp_max(dm);
+    __threadfence();
+    if ((threadIdx.x & 31) == 0) cluster.map_shared_rank(red, 0)[cF.Wg] = dm;
+    cluster.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      double d = 0.0;
+      for (int w = 0; w < nW; ++w) d = fmax(d, red[w]);
+      A.last_delta[i] = d;
+      A.vrem[i] = v;
+      A.consumed[i] = v;
+      A.stable[i] = fonly ? 1 : 0;
+      A.counts[i] += 1;
+      const long long ev = (long long)atomicAdd((unsigned long long *)A.events, 1ull) + 1;
+      __threadfence();
+      st_release_s64(A.ver + i, vi + 1);
+      atomicExch(A.busy + i, 0);
+      if (async_done(A)) atomicExch(A.stop, 1);
+      else if (ev >= A.max_events) atomicCAS(A.stop, 0, 2);
+    }
+  }
+  if (bad) atomicExch(A.nonfinite, 1);
+  cluster.sync();
+}
+
+extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
+                              int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
+                              int64_t *counts_out, int64_t *info_out, void *stream) {
+  if (!fine || !coarse) return PINT_EARG;
+  pint_ctx *ctx = fine->ctx;
+  try {
+    if (fine->desc.ndim != 1 || coarse->desc.ndim != 1 || fine->desc.rule == PINT_RULE_FORWARD_EULER ||
+        coarse->desc.rule == PINT_RULE_FORWARD_EULER)
+      pint_throw(PINT_EUNSUPPORTED, "the device async runtime supports 1-D implicit fine and coarse operators");
+    const Tri1DPlan &pf = fine->plan, &pg = coarse->plan;
+    if (pf.N != pg.N || pf.CH != pg.CH || pf.T != pg.T)
+      pint_throw(PINT_EUNSUPPORTED, "fine and coarse operators must share the register layout (same rule family)");
+    if (p < 1 || !lam0 || !final_out) pint_throw(PINT_EARG, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t N = pf.N;
+    const int R = 3;
+    const int CL = fine->batch_cluster;
+    const int TB = pf.T / CL;
+    int dev_sms = ctx->num_sms;
+    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(p, dev_sms / CL));
+    // device workspace
+    size_t bytes = 0;
+    auto take = [&](size_t n) { size_t o = bytes; bytes += (n + 255) / 256 * 256; return o; };
+    const size_t o_ring = take(sizeof(double) * (p + 1) * R * N), o_remb = take(sizeof(double) * (p + 1) * N),
+                 o_gremb = take(sizeof(double) * (p + 1) * N), o_scr = take(sizeof(double) * ncl * 2 * N),
+                 o_ver = take(8 * (p + 1)), o_vrem = take(8 * (p + 1)), o_cons = take(8 * (p + 1)),
+                 o_busy = take(4 * (p + 1)), o_stab = take(4 * (p + 1)), o_cnt = take(8 * (p + 1)),
+                 o_ld = take(8 * (p + 1)), o_misc = take(64);
+    char *w = nullptr;
+    PINT_CUDA(cudaMallocAsync((void **)&w, bytes, s));
+    PINT_CUDA(cudaMemsetAsync(w + o_ver, 0, o_misc + 64 - o_ver, s));
+    AsyncArgs A;
+    A.ring = (double *)(w + o_ring);
+    A.remb = (double *)(w + o_remb);
+    A.gremb = (double *)(w + o_gremb);
+    A.scratch = (double *)(w + o_scr);
+    A.ver = (long long *)(w + o_ver);
+    A.vrem = (long long *)(w + o_vrem);
+    A.consumed = (long long *)(w + o_cons);
+    A.busy = (int *)(w + o_busy);
+    A.stable = (int *)(w + o_stab);
+    A.counts = (long long *)(w + o_cnt);
+    A.last_delta = (double *)(w + o_ld);
+    A.ticket = (unsigned long long *)(w + o_misc);
+    A.stop = (int *)(w + o_misc + 8);
+    A.nonfinite = (int *)(w + o_misc + 12);
+    A.events = (long long *)(w + o_misc + 16);
+    A.retries = (long long *)(w + o_misc + 24);
+    A.P = p;
+    A.N = N;
+    A.R = R;
+    A.eps = epsilon;
+    A.max_events = max_events > 0 ? max_events : 20000;
+    A.delay_frac = delay_frac;
+    A.seed = seed;
+    // initial versions: ring[i][0] = lam0[i]; remembered = lam0[i-1] (version 0);
+    // G(remembered) = G(lam0[i-1]) = lam0[i] (coarse initial iterate)
+    const double *L = (const double *)lam0;
+    for (int64_t i = 0; i <= p; ++i)
+      PINT_CUDA(cudaMemcpyAsync(A.ring + (size_t)i * R * N, L + i * N, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    PINT_CUDA(cudaMemcpyAsync(A.remb + N, L, sizeof(double) * p * N, cudaMemcpyDeviceToDevice, s));
+    PINT_CUDA(cudaMemcpyAsync(A.gremb + N, L + N, sizeof(double) * p * N, cudaMemcpyDeviceToDevice, s));
+    {
+      std::vector<double> inf(p + 1, INFINITY);
+      inf[0] = 0.0;
+      std::vector<long long> minus1(p + 1, -1);
+      PINT_CUDA(cudaMemcpyAsync(A.last_delta, inf.data(), 8 * (p + 1), cudaMemcpyHostToDevice, s));
+      PINT_CUDA(cudaMemcpyAsync(A.consumed, minus1.data(), 8 * (p + 1), cudaMemcpyHostToDevice, s));
+      PINT_CUDA(cudaStreamSynchronize(s));
+    }
+    const size_t sm = sizeof(double) * (2 * (size_t)tri1d_nfields(pf.J) * TB + 8 * (size_t)(pf.nW + 1)) + 16 +
+                      64 + 32 * 8 * 4;
+    const bool general = pf.tb < pf.T || pf.f_first != 0.0 || pf.f_last != 0.0 || pg.f_first != 0.0 ||
+                         pg.f_last != 0.0;
+#define PINT_ASYNC_LAUNCH(CHV, JV, CNF, CNG, GV)                                                        \
+  launch_cluster(tri1d_async_kernel<CHV, JV, CNF, CNG, GV>, (int)(ncl * CL), TB, CL, sm, s,              \
+                 make_params<CHV>(fine), make_params<CHV>(coarse), A)
+#define PINT_ASYNC_J(CHV, CNF, CNG, GV)                      \
+  switch (pf.J) {                                            \
+    case 1: PINT_ASYNC_LAUNCH(CHV, 1, CNF, CNG, GV); break;  \
+    case 2: PINT_ASYNC_LAUNCH(CHV, 2, CNF, CNG, GV); break;  \
+    default: PINT_ASYNC_LAUNCH(CHV, 4, CNF, CNG, GV); break; \
+  }
+    if (pf.CH == 16) {
+      if (pf.cn && pg.cn) {
+        if (general) { PINT_ASYNC_J(16, true, true, true) } else { PINT_ASYNC_J(16, true, true, false) }
+      } else if (pf.cn) {
+        if (general) { PINT_ASYNC_J(16, true, false, true) } else { PINT_ASYNC_J(16, true, false, false) }
+      } else if (!pg.cn) {
+        if (general) { PINT_ASYNC_J(16, false, false, true) } else { PINT_ASYNC_J(16, false, false, false) }
+      } else {
+        pint_throw(PINT_EUNSUPPORTED, "backward-Euler fine with trapezoidal coarse is not fused in the device runtime");
+      }
+    } else {
+      if (general) { PINT_ASYNC_J(32, false, false, true) } else { PINT_ASYNC_J(32, false, false, false) }
+    }
+#undef PINT_ASYNC_J
+#undef PINT_ASYNC_LAUNCH
+    // gather the newest published version of every slice
+    std::vector<long long> ver(p + 1), cnt(p + 1);
+    long long misc[4];
+    int flags[2];
+    PINT_CUDA(cudaMemcpyAsync(ver.data(), A.ver, 8 * (p + 1), cudaMemcpyDeviceToHost, s));
+    PINT_CUDA(cudaMemcpyAsync(cnt.data(), A.counts, 8 * (p + 1), cudaMemcpyDeviceToHost, s));
+    PINT_CUDA(cudaMemcpyAsync(flags, A.stop, 8, cudaMemcpyDeviceToHost, s));
+    PINT_CUDA(cudaMemcpyAsync(misc, A.events, 16, cudaMemcpyDeviceToHost, s));
+    PINT_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i <= p; ++i)
+      PINT_CUDA(cudaMemcpyAsync((double *)final_out + i * N, A.ring + ((size_t)i * R + (size_t)(ver[i] % R)) * N,
+                                sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    PINT_CUDA(cudaFreeAsync(w, s));
+    PINT_CUDA(cudaStreamSynchronize(s));
+    if (counts_out)
+      for (int64_t i = 0; i <= p; ++i) counts_out[i] = cnt[i];
+    if (info_out) {
+      info_out[0] = misc[0];   // events (activations)
+      info_out[1] = flags[0];  // 1 converged, 2 max_events
+      info_out[2] = flags[1];  // non-finite
+      info_out[3] = misc[1];   // seqlock retries
+      info_out[4] = ncl;       // concurrent clusters
+    }
+    return PINT_OK;
+  } catch (const PintError &e) {
+    ctx->last_error = e.msg;
+    ctx->last_value = e.value;
     return e.code;
   }
 }

@@ -445,3 +445,16 @@ PROPAGATOR_RULES = {
     "trapezoidal": trapezoidal_propagator,
     "forward-euler": forward_euler_propagator,
 }
+
+
+def with_register_layout(prop: GPUPropagator, points_per_thread: int) -> GPUPropagator:
+    """The same operator built with another register layout (1-D implicit
+    operators: 16 or 32 points per thread). Used to pair a backward-Euler
+    coarse operator with a trapezoidal fine operator inside one persistent
+    kernel; values agree with ``prop`` to rounding, not bitwise."""
+    if prop.info.points_per_thread == points_per_thread:
+        return prop
+    d = _native.OpDesc()
+    ctypes.memmove(ctypes.byref(d), ctypes.byref(prop.desc), ctypes.sizeof(d))
+    d.layout_ch = int(points_per_thread)
+    return GPUPropagator(d, prop.dim, prop.dtype, prop.cost_units, prop.device, prop.rule, prop.span, prop.steps)

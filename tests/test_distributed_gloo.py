@@ -1,0 +1,99 @@
+"""Multi-rank synchronous Parareal protocol (paper_2110_10762_b200/distributed.py)
+on CPU: world_size 2 and 3 over gloo, with an oracle-backed test double of the
+per-rank device engine. The sharded run must reproduce the single-process
+run bitwise (same k, stop reason, deltas, iterate)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import heat_oracle as H
+
+
+class CPUEngine:
+    """Same interface as parareal.SyncEngine, numpy oracle propagators."""
+
+    def __init__(self, coarse, fine, p):
+        n = fine.n
+        self.coarse, self.fine, self.p = coarse, fine, p
+        z = lambda: torch.zeros(p + 1, n, dtype=torch.float64)  # noqa: E731
+        self.lam_a, self.lam_b, self.fv, self.gcache = z(), z(), z(), z()
+        self.deltas = torch.zeros(p + 1, dtype=torch.float64)
+        self.dmax = torch.zeros(1, dtype=torch.float64)
+        self.flag = torch.zeros(1, dtype=torch.int32)
+        self.prev = self.lam_a
+
+    def init(self, u0):
+        self.lam_a[0] = torch.as_tensor(np.asarray(u0, dtype=float))
+        self.lam_b[0] = self.lam_a[0]
+        for i in range(1, self.p + 1):
+            self.lam_a[i] = torch.from_numpy(self.coarse.apply(self.lam_a[i - 1].numpy()))
+        self.gcache.copy_(self.lam_a)
+        self.prev = self.lam_a
+
+    def fine_batch(self, k, fine_done_event=None):
+        self.fv[k:] = torch.from_numpy(self.fine.apply_batch(self.prev[k - 1:self.p].numpy()))
+
+    def coarse_sweep(self, k, nxt, chain_in=False):
+        prev = self.prev
+        if not chain_in:
+            nxt[k - 1] = prev[k - 1]
+            self.deltas[k - 1] = 0.0
+        for i in range(k, self.p + 1):
+            g = torch.from_numpy(self.coarse.apply(nxt[i - 1].numpy()))
+            fonly = (float(self.deltas[i - 1]) == 0.0) if (chain_in or i > k) else True
+            v = self.fv[i].clone() if fonly else (g + self.fv[i]) - self.gcache[i]
+            self.deltas[i] = float((v - prev[i]).abs().max())
+            self.gcache[i] = g
+            nxt[i] = v
+
+    def reduce_delta(self, k):
+        self.dmax[0] = self.deltas[k - 1:].max()
+
+    def launches_per_sweep(self):
+        return 0
+
+
+def problem(n=64):
+    a_d, a_o, c = H.heat1d_coeffs(n, 1.0, 0.5, -0.25)
+    return H.Tridiag1D(n, a_d, a_o, c, 0.05, 1), H.Tridiag1D(n, a_d, a_o, c, 0.05, 20), H.sine_u0_1d(n, 8, 0)
+
+
+def _worker(rank, world, port, p_local, eps, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_10762_b200 import distributed as D
+    coarse, fine, u0 = problem()
+    res = D.run_parareal_sharded(coarse, fine, u0, p_local, eps, engine=CPUEngine(coarse, fine, p_local))
+    shards = [torch.zeros_like(res["shard"]) for _ in range(world)]
+    dist.all_gather(shards, res["shard"])
+    if rank == 0:
+        full = torch.cat([shards[0]] + [s[1:] for s in shards[1:]]).numpy()
+        np.savez(out, full=full, k=res["k_final"], stop=res["stop_reason"], deltas=np.array(res["deltas"]))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world,p_local,eps", [(2, 4, 1e-9), (3, 3, 0.0), (2, 5, 1e-4)])
+def test_sharded_run_equals_single_process(tmp_path, world, p_local, eps):
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), p_local, eps, out), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    coarse, fine, u0 = problem()
+    ref = H.run_parareal(coarse, fine, u0, p_local * world, eps)
+    assert int(got["k"]) == ref.k_final
+    assert str(got["stop"]) == ref.stop_reason
+    assert np.array_equal(got["deltas"], np.array(ref.deltas))
+    assert np.array_equal(got["full"], ref.iterates[-1])

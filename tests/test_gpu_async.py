@@ -95,3 +95,42 @@ def test_c1_async_reaches_the_sync_solution(gpu):
     _, kappa = gpu.update_counts(tr)
     sync = gpu.run_parareal(coarse, fine, u0, p, 1e-10)
     assert kappa >= sync.k_final
+
+
+# ------------------------------------------------ device runtime (real async)
+@pytest.mark.parametrize("delay", [0.0, 0.2])
+def test_device_async_quiescence_is_the_sequential_solution(gpu, delay):
+    """Real concurrency: exact quiescence lands on the sequential fine solution
+    bitwise (finite termination)."""
+    from oracle import heat_oracle as H
+    n, p = 1024, 16
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 100)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, delay_frac=delay, seed=7)
+    assert res.stop_reason == "converged"
+    assert np.array_equal(res.final.data, seq)
+    assert res.kappa >= 1 and res.activations >= p
+
+
+def test_device_async_epsilon_stop_reaches_sync_solution(gpu):
+    from oracle import heat_oracle as H
+    n, p = 1024, 16
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 100)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, 1e-10)
+    assert res.stop_reason == "converged"
+    assert np.max(np.abs(res.final.data - seq)) < 1e-8
+
+
+def test_device_async_fixture_with_boundary_forcing(gpu):
+    ivp, coarse, fine = heat_pair(gpu, 8)
+    for p in (3, 7):
+        seq = gpu.sequential_fine_solve(fine, ivp.u0, p).data
+        res = gpu.run_async_parareal_device(coarse, fine, ivp.u0, p, None, seed=p)
+        assert np.array_equal(res.final.data, seq)
