@@ -350,6 +350,19 @@ __device__ __forceinline__ double lds(uint32_t a) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
+// Non-volatile shared load: free to be scheduled (and CSE'd) within a step;
+// its address comes from opaque() once per step so it is never hoisted out of
+// the step loop into (spilled) registers.
+__device__ __forceinline__ double lds_free(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
@@ -398,7 +411,7 @@ __device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t s
   return gb;
 }
 
-#define TAB(f) lds(c.tab + (uint32_t)(f) * 8u)
+#define TAB(f) lds_free(tab + (uint32_t)(f) * 8u)
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -418,6 +431,7 @@ template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool 
 __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
                                          uint32_t sc, double extra_in, double *extra_out) {
   const bool regular = !GENERAL || c.t < P.tb;
+  const uint32_t tab = opaque(c.tab);
   double xo[CN ? CH : 1];
   if (CN) {
 #pragma unroll
@@ -460,7 +474,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double gP = shfl_d(pw, 31);
   const double gQ = shfl_d(y1, 0);
   const double gZ = shfl_d(y0, 0);
-  const uint32_t gb = gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in);
+  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in));
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
 #pragma unroll
@@ -469,18 +483,26 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     double B = 0.0;
     if (V < c.nW) {
       const uint32_t o = (uint32_t)V * 8u;
-      B = fma(-TAB(TF_R2 + 3 * J + j), lds(gb + stride8 + o + 8u),
-              fma(-TAB(TF_R2 + 2 * J + j), lds(gb + 2u * stride8 + o + 8u), lds(gb + o)));
-      if (WITH_EXTRA) ex = fmax(ex, lds(gb + 3u * stride8 + o));
+      B = fma(-TAB(TF_R2 + 3 * J + j), lds_free(gb + stride8 + o + 8u),
+              fma(-TAB(TF_R2 + 2 * J + j), lds_free(gb + 2u * stride8 + o + 8u), lds_free(gb + o)));
+      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 3u * stride8 + o));
     }
     sl = fma(TAB(TF_R2 + j), B, sl);
     sr = fma(TAB(TF_R2 + J + j), B, sr);
   }
+  // split butterfly: the lower half-warp reduces sl, the upper half sr
+  {
+    const bool lo = c.lane < 16;
+    double keep = lo ? sl : sr;
+    keep += __shfl_xor_sync(FULLMASK, lo ? sr : sl, 16);
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    sl += __shfl_xor_sync(FULLMASK, sl, o);
-    sr += __shfl_xor_sync(FULLMASK, sr, o);
-    if (WITH_EXTRA) ex = fmax(ex, __shfl_xor_sync(FULLMASK, ex, o));
+    for (int o = 8; o >= 1; o >>= 1) keep += __shfl_xor_sync(FULLMASK, keep, o);
+    sl = __shfl_sync(FULLMASK, keep, 0);
+    sr = __shfl_sync(FULLMASK, keep, 16);
+  }
+  if (WITH_EXTRA) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ex = fmax(ex, __shfl_xor_sync(FULLMASK, ex, o));
   }
   if (WITH_EXTRA) *extra_out = ex;
   double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
