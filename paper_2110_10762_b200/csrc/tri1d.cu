@@ -676,24 +676,40 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   double dpart = 0.0;  // warp-uniform partial max of the previous slice
   bool bad = false;
   const int64_t base = (int64_t)c.t * CH;
-  // this thread's private staging row for F(old), G(old), prev of the slice
-  // being corrected: filled by cp.async while the coarse step runs
-  const uint32_t row = smem_u32(smem + (15 + 4 * J) * c.TB + 8 * (c.nW + 1) + 2) +
-                       (uint32_t)threadIdx.x * (uint32_t)(3 * CH + 2) * 8u;
-  const int64_t rem_ = N - base;
-  const int nvalid = rem_ <= 0 ? 0 : (rem_ >= CH ? CH : (int)rem_);
-  const bool vec16 = ((N & 1) == 0) && nvalid == CH;
+  // Per-thread staging rows in shared memory, [F(old) | G(old) | prev] x CH
+  // doubles + 16 B pad (stride 784 B: 16-byte accesses of 8 consecutive lanes
+  // hit distinct banks). The warp fills them with coalesced cp.async while
+  // the coarse step runs (lane l copies 16 B of the warp's contiguous
+  // 32*CH-point segment into whichever row owns it), and writes the new
+  // iterate and G(new) back the same way after the correction.
+  const uint32_t RS = (uint32_t)(3 * CH + 2) * 8u;  // row stride in bytes
+  const uint32_t row = smem_u32(smem + (15 + 4 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
+  const uint32_t wrow0 = row - (uint32_t)c.lane * RS;  // lane 0's row
+  const int64_t wbase = (int64_t)(c.t - c.lane) * CH;  // warp segment start (points)
+  const bool even = (N & 1) == 0;
+  double nanacc = 0.0;
   for (int64_t i = k; i <= p; ++i) {
     {
-      const double *srcs[3] = {fv + i * N + base, gcache + i * N + base, prev + i * N + base};
+      const double *srcs[3] = {fv + i * N + wbase, gcache + i * N + wbase, prev + i * N + wbase};
+      if (even) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const uint32_t dst = row + (uint32_t)(a * CH) * 8u;
-        if (vec16) {
+        for (int kk = 0; kk < CH / 2; ++kk) {
+          const int e = kk * 64 + 2 * c.lane;
+          const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+          if (wbase + e < N) {
 #pragma unroll
-          for (int j = 0; j < CH; j += 2) cp_async16(dst + j * 8u, srcs[a] + j);
-        } else {
-          for (int j = 0; j < nvalid; ++j) cp_async8(dst + j * 8u, srcs[a] + j);
+            for (int a = 0; a < 3; ++a) cp_async16(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < CH; ++kk) {
+          const int e = kk * 32 + c.lane;
+          const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+          if (wbase + e < N) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) cp_async8(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
+          }
         }
       }
       cp_async_commit();
@@ -702,27 +718,65 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, dpart, &dprev);
     if (i > k && rank == 0 && threadIdx.x == 0) deltas[i - 1] = dprev;
     const bool fonly = (i == k) ? (delta_in == 0.0) : (dprev == 0.0);
-    double *gw = gcache + i * N + base;
-    double *nw = next + i * N + base;
     cp_async_wait_all();
+    __syncwarp();
+    const uint32_t r = opaque(row);
     double dm = 0.0;
+    double gprev = 0.0, vprev = 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
+      double v = 0.0;
+      const double g = x[j];
       if (base + j < N) {
-        const double g = x[j];
-        const double fj = lds(row + (uint32_t)j * 8u);
-        const double v = fonly ? fj : (g + fj) - lds(row + (uint32_t)(CH + j) * 8u);
-        dm = fmax(dm, fabs(v - lds(row + (uint32_t)(2 * CH + j) * 8u)));
-        bad |= !isfinite(v);
-        gw[j] = g;
-        nw[j] = v;
-        x[j] = v;
+        const double fj = lds_free(r + (uint32_t)j * 8u);
+        v = fonly ? fj : (g + fj) - lds_free(r + (uint32_t)(CH + j) * 8u);
+        dm = fmax(dm, fabs(v - lds_free(r + (uint32_t)(2 * CH + j) * 8u)));
+        nanacc += v - v;  // NaN iff v is not finite
+      }
+      x[j] = v;
+      if (j & 1) {  // stage (new, G(new)) pairs into the F / G(old) slots of the own row
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(j - 1) * 8u), "d"(vprev), "d"(v)
+                     : "memory");
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(CH + j - 1) * 8u), "d"(gprev),
+                     "d"(g) : "memory");
       } else {
-        x[j] = 0.0;
+        vprev = v;
+        gprev = g;
       }
     }
+    __syncwarp();
+    {
+      double *dsts[2] = {next + i * N + wbase, gcache + i * N + wbase};
+      if (even) {
+#pragma unroll
+        for (int kk = 0; kk < CH / 2; ++kk) {
+          const int e = kk * 64 + 2 * c.lane;
+          const uint32_t src = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+          if (wbase + e < N) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+              double2 v2;
+              asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v2.x), "=d"(v2.y) : "r"(src + (uint32_t)(a * CH) * 8u));
+              *reinterpret_cast<double2 *>(dsts[a] + e) = v2;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < CH; ++kk) {
+          const int e = kk * 32 + c.lane;
+          const uint32_t src = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+          if (wbase + e < N) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a) dsts[a][e] = lds(src + (uint32_t)(a * CH) * 8u);
+          }
+        }
+      }
+    }
+    __syncwarp();  // the rows are refilled by the next slice's cp.async
     dpart = warp_max(dm);
   }
+  if (nanacc != nanacc) bad = true;
   // final reduction for slice p through one more gather round
   {
     const uint32_t gb = gather_exchange<4>(c, sc, 0.0, 0.0, 0.0, dpart);
