@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pint_internal.cuh"
 
@@ -172,11 +173,20 @@ void stencil_setup(pint_op *op) {
   if (op->nx > maxint || op->ny > maxint || op->nz > maxint) pint_throw(PINT_EDIM, "grid too large");
 }
 
+template <typename T>
+void fe2d_wave_apply(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride, cudaStream_t st);
+template <typename T>
+void fe3d_wave_apply(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride, cudaStream_t st);
+
 void stencil_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch, int64_t stride, cudaStream_t s) {
   const int64_t S = op->desc.steps;
   const int nd = op->desc.ndim;
   const int esz = op->desc.dtype == PINT_F64 ? 8 : 4;
-  const int sblk = nd == 1 ? fused_steps<1>(esz) : (nd == 2 ? fused_steps<2>(esz) : fused_steps<3>(esz));
+  int sblk = nd == 1 ? fused_steps<1>(esz) : (nd == 2 ? fused_steps<2>(esz) : fused_steps<3>(esz));
+  const bool v1 = getenv("PINT_STENCIL_V1") && atoi(getenv("PINT_STENCIL_V1"));
+  const bool wave2 = nd == 2 && !v1, wave3 = nd == 3 && !v1;
+  if (wave2) sblk = 8;
+  if (wave3) sblk = 4;
   void *scratch = nullptr;
   if (S > sblk) {
     const size_t need = (size_t)nbatch * stride * esz;
@@ -188,6 +198,20 @@ void stencil_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
       op->cg_work_bytes = need;
     }
     scratch = op->cg_work;
+  }
+  if (wave3) {
+    if (op->desc.dtype == PINT_F64)
+      fe3d_wave_apply<double>(op, (const double *)in, (double *)out, (double *)scratch, nbatch, stride, s);
+    else
+      fe3d_wave_apply<float>(op, (const float *)in, (float *)out, (float *)scratch, nbatch, stride, s);
+    return;
+  }
+  if (wave2) {
+    if (op->desc.dtype == PINT_F64)
+      fe2d_wave_apply<double>(op, (const double *)in, (double *)out, (double *)scratch, nbatch, stride, s);
+    else
+      fe2d_wave_apply<float>(op, (const float *)in, (float *)out, (float *)scratch, nbatch, stride, s);
+    return;
   }
   if (op->desc.dtype == PINT_F64) {
     if (nd == 1) fe_launch<double, 1>(op, (const double *)in, (double *)out, (double *)scratch, nbatch, stride, s);
