@@ -64,6 +64,12 @@ enum pint_status {
 
 enum pint_dtype { PINT_F32 = 0, PINT_F64 = 1 };
 
+/* Solver of the 2-D/3-D implicit (backward-Euler) step. */
+enum pint_nd_solver {
+  PINT_ND_DIRECT = 0, /* sine-transform diagonalisation + tridiagonal sweeps: exact to rounding */
+  PINT_ND_CG = 1      /* conjugate gradients to ||r|| <= cg_rtol ||b||                        */
+};
+
 enum pint_rule {
   PINT_RULE_BACKWARD_EULER = 0, /* (I - dt A) u+ = u + dt c                */
   PINT_RULE_TRAPEZOIDAL = 1,    /* (I - dt/2 A) u+ = (I + dt/2 A) u + dt c */
@@ -83,14 +89,16 @@ typedef struct pint_op pint_op;
  *              c[n-1] = c_last (summed when n == 1).
  *   ndim >= 2: A = (1/h^2) * (zero-Dirichlet 5/7-point Laplacian), c = 0.
  * One propagator application advances `steps` steps of width dt = span/steps.
- * Implicit rules in 2-D/3-D are solved by conjugate gradients to
- * ||r||_2 <= cg_rtol * ||b||_2 (at most cg_maxit iterations).
+ * Implicit rules in 2-D/3-D are solved directly (nd_solver = PINT_ND_DIRECT,
+ * the default: same system as the reference's dense LU solve, model.py:157-184)
+ * or by conjugate gradients to ||r||_2 <= cg_rtol * ||b||_2 (at most cg_maxit
+ * iterations; nd_solver = PINT_ND_CG).
  */
 typedef struct pint_op_desc {
   int32_t ndim;
   int32_t rule;      /* enum pint_rule */
   int32_t dtype;     /* enum pint_dtype */
-  int32_t reserved0;
+  int32_t nd_solver; /* enum pint_nd_solver (ndim >= 2 implicit) */
   int64_t shape[3];
   double h;          /* grid spacing (ndim >= 2) */
   double span;       /* time covered by one application */

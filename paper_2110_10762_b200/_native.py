@@ -41,7 +41,7 @@ c_double = ctypes.c_double
 
 class OpDesc(ctypes.Structure):
     _fields_ = [
-        ("ndim", c_i32), ("rule", c_i32), ("dtype", c_i32), ("reserved0", c_i32),
+        ("ndim", c_i32), ("rule", c_i32), ("dtype", c_i32), ("nd_solver", c_i32),
         ("shape", c_i64 * 3), ("h", c_double), ("span", c_double), ("steps", c_i64),
         ("a_diag", c_double), ("a_off", c_double), ("c_first", c_double), ("c_last", c_double),
         ("cg_rtol", c_double), ("cg_maxit", c_i64), ("layout_ch", c_i32), ("reserved1", c_i32),

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libpint_b200.so")
 STAMP = LIB + ".srchash"
 
-SOURCES = ["abi.cu", "tri1d.cu", "correct.cu", "stencil.cu", "stencil_wave.cu", "cg.cu"]
+SOURCES = ["abi.cu", "tri1d.cu", "correct.cu", "stencil.cu", "stencil_wave.cu", "cg.cu", "spectral.cu"]
 HEADERS = ["pint_internal.cuh", os.path.join("..", "..", "include", "pint_abi.h")]
 
 NVCC_FLAGS = [

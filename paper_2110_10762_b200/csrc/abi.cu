@@ -115,7 +115,11 @@ int pint_op_create(pint_ctx *ctx, const pint_op_desc *desc, pint_op **out) {
       op->ny = d.ndim >= 2 ? d.shape[d.ndim - 2] : 1;
       op->nz = d.ndim >= 3 ? d.shape[0] : 1;
       if (d.rule == PINT_RULE_FORWARD_EULER) stencil_setup(op);
-      else if (d.rule == PINT_RULE_BACKWARD_EULER) cg_setup(op);
+      else if (d.rule == PINT_RULE_BACKWARD_EULER) {
+        if (d.nd_solver == PINT_ND_CG) cg_setup(op);
+        else if (d.nd_solver == PINT_ND_DIRECT) spectral_setup(op);
+        else pint_throw(PINT_EARG, "nd_solver must be PINT_ND_DIRECT or PINT_ND_CG");
+      }
       else pint_throw(PINT_EUNSUPPORTED, "trapezoidal rule is implemented for 1-D operators only");
     }
   });
@@ -174,7 +178,7 @@ int pint_op_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch, 
     if (a < b + span && b < a + span) pint_throw(PINT_EARG, "in and out must not alias");
     cudaStream_t s = (cudaStream_t)stream;
     if (is_tri1d(op)) tri1d_apply_batch(op, (const double *)in, (double *)out, nbatch, stride, s);
-    else if (is_cg(op)) cg_apply_batch(op, in, out, nbatch, stride, s);
+    else if (is_cg(op)) nd_implicit_apply_batch(op, in, out, nbatch, stride, s);
     else stencil_apply_batch(op, in, out, nbatch, stride, s);
   });
 }
@@ -208,7 +212,7 @@ int pint_coarse_init(pint_op *coarse, void *lam, int64_t p, void *gcache, void *
     const int64_t n = coarse->dim;
     char *base = (char *)lam;
     for (int64_t i = 1; i <= p; ++i) {
-      if (is_cg(coarse)) cg_apply_batch(coarse, base + (i - 1) * n * esz, base + i * n * esz, 1, n, s);
+      if (is_cg(coarse)) nd_implicit_apply_batch(coarse, base + (i - 1) * n * esz, base + i * n * esz, 1, n, s);
       else stencil_apply_batch(coarse, base + (i - 1) * n * esz, base + i * n * esz, 1, n, s);
     }
     if (gcache)

@@ -226,7 +226,14 @@ void cg_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch, int6
   }
 }
 
+void nd_implicit_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch, int64_t stride,
+                             cudaStream_t s) {
+  if (op->desc.nd_solver == PINT_ND_CG) cg_apply_batch(op, in, out, nbatch, stride, s);
+  else spectral_apply_batch(op, in, out, nbatch, stride, s);
+}
+
 void nd_destroy(pint_op *op) {
+  spectral_destroy(op);
   if (op->cg_work) cudaFree(op->cg_work);
   if (op->cg_partials) cudaFree(op->cg_partials);
   op->cg_work = nullptr;

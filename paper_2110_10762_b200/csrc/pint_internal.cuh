@@ -95,6 +95,8 @@ struct pint_op {
   double *cg_partials = nullptr;
   int64_t cg_nblocks = 0;
   int64_t cg_last_iters = 0;
+  void *spec_q = nullptr;      // direct solve: n x n sine transform (T)
+  double *spec_mu = nullptr;   // direct solve: 1-D Laplacian eigenvalues * h^2
 };
 
 // 1-D launchers (tri1d.cu)
@@ -116,6 +118,13 @@ void cg_setup(pint_op *op);
 void cg_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
                     int64_t stride, cudaStream_t s);
 void nd_destroy(pint_op *op);
+void spectral_setup(pint_op *op);
+void spectral_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
+                          int64_t stride, cudaStream_t s);
+void spectral_destroy(pint_op *op);
+// 2-D/3-D implicit coarse apply: direct (spectral) or CG per desc.nd_solver
+void nd_implicit_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
+                             int64_t stride, cudaStream_t s);
 
 // elementwise (correct.cu)
 void correct_launch(int dtype, int64_t dim, int64_t nbatch, const void *gnew,

@@ -369,8 +369,13 @@ class GPUPropagator:
         return _device.to_host((cols - z).T).astype(float)
 
 
+# 2-D/3-D implicit step: "direct" = sine-transform diagonalisation (exact to
+# rounding, as the reference's dense LU); "cg" = conjugate gradients to cg_rtol.
+ND_SOLVERS = {"direct": 0, "cg": 1}
+
+
 def _build(ivp, span: float, steps: int, rule: str, *, dtype=None, device=None,
-           cg_rtol: float | None = None, cg_maxit: int = 10_000) -> GPUPropagator:
+           cg_rtol: float | None = None, cg_maxit: int = 10_000, solver: str = "direct") -> GPUPropagator:
     if steps < 1:
         raise ValueError(f"step count must be >= 1, got {steps}")
     if not span > 0.0:
@@ -395,6 +400,9 @@ def _build(ivp, span: float, steps: int, rule: str, *, dtype=None, device=None,
             cg_rtol = 1e-12 if tdt == torch.float64 else 1e-6
         d.cg_rtol = float(cg_rtol)
         d.cg_maxit = int(cg_maxit)
+        if solver not in ND_SOLVERS:
+            raise ValueError(f"solver must be one of {sorted(ND_SOLVERS)}, got {solver!r}")
+        d.nd_solver = ND_SOLVERS[solver]
         dim = ivp.dim
     else:
         if rule == "forward-euler":

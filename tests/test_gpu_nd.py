@@ -1,5 +1,5 @@
-"""GPU parity of the 2-D/3-D explicit stencil (fine) and CG implicit (coarse)
-propagators and of synchronous Parareal on the reduced C3/C4 analogs, against
+"""GPU parity of the 2-D/3-D explicit stencil (fine) and implicit (coarse:
+direct sine-transform solve, and CG) propagators and of synchronous Parareal on the reduced C3/C4 analogs, against
 golden vectors from the reference's dense route and the numpy oracle."""
 import json
 
@@ -12,7 +12,7 @@ from oracle import heat_oracle as H
 pytestmark = pytest.mark.gpu
 
 
-def _setup(gpu, tag, dtype="float64", cg_rtol=None):
+def _setup(gpu, tag, dtype="float64", cg_rtol=None, solver="direct"):
     g = golden("reduced_nd.npz")
     meta = json.loads(str(g[f"{tag}_meta"]))
     shape = tuple(meta["shape"])
@@ -23,14 +23,15 @@ def _setup(gpu, tag, dtype="float64", cg_rtol=None):
     mk = gpu.heat2d_system if len(shape) == 2 else gpu.heat3d_system
     ivp = mk(n, t_final=p * span, u0=u0)
     fine = gpu.forward_euler_propagator(ivp, span, meta["steps"], dtype=dtype)
-    kw = {} if cg_rtol is None else {"cg_rtol": cg_rtol}
+    kw = {"solver": solver} if cg_rtol is None else {"cg_rtol": cg_rtol, "solver": solver}
     coarse = gpu.backward_euler_propagator(ivp, span, 1, dtype=dtype, **kw)
     return g, meta, ivp, fine, coarse, u0
 
 
+@pytest.mark.parametrize("solver", ("direct", "cg"))
 @pytest.mark.parametrize("tag", ("2d", "3d"))
-def test_reduced_nd_sync_parareal_matches_reference(gpu, tag):
-    g, meta, ivp, fine, coarse, u0 = _setup(gpu, tag)
+def test_reduced_nd_sync_parareal_matches_reference(gpu, tag, solver):
+    g, meta, ivp, fine, coarse, u0 = _setup(gpu, tag, solver=solver)
     tr = gpu.run_parareal(coarse, fine, u0, meta["p"], meta["eps"])
     assert tr.k_final == int(g[f"{tag}_k"])
     assert tr.stop_reason == str(g[f"{tag}_stop"])
@@ -40,9 +41,10 @@ def test_reduced_nd_sync_parareal_matches_reference(gpu, tag):
     assert rel_l2(seq.data, g[f"{tag}_seq"]) < 1e-11
 
 
+@pytest.mark.parametrize("solver", ("direct", "cg"))
 @pytest.mark.parametrize("tag", ("2d", "3d"))
-def test_reduced_nd_fp32_within_1e5(gpu, tag):
-    g, meta, ivp, fine, coarse, u0 = _setup(gpu, tag, dtype="float32")
+def test_reduced_nd_fp32_within_1e5(gpu, tag, solver):
+    g, meta, ivp, fine, coarse, u0 = _setup(gpu, tag, dtype="float32", solver=solver)
     tr = gpu.run_parareal(coarse, fine, u0, meta["p"], 1e-6)
     ref = g[f"{tag}_seq"]
     assert rel_l2(tr.final.data, ref) < 1e-5
@@ -72,8 +74,10 @@ def test_explicit_stencil_matches_oracle(gpu, shape, steps, cfl):
         assert torch.equal(out[0], fine.apply(xs[0]))
 
 
-@pytest.mark.parametrize("shape", [(64, 64), (20, 20, 20)])
-def test_cg_coarse_matches_direct_solve(gpu, shape):
+@pytest.mark.parametrize("solver,tol", [("direct", 1e-13), ("cg", 1e-11)])
+@pytest.mark.parametrize("shape,steps", [((64, 64), 1), ((20, 20, 20), 1), ((37, 37), 3), ((9, 9, 9), 2),
+                                         ((1, 1), 1), ((2, 2, 2), 1), ((130, 130), 1)])
+def test_implicit_coarse_matches_sparse_lu(gpu, shape, steps, solver, tol):
     n = shape[0]
     h = 1.0 / (n + 1)
     dT = 50 * h * h
@@ -81,20 +85,68 @@ def test_cg_coarse_matches_direct_solve(gpu, shape):
     u = rng.standard_normal(int(np.prod(shape)))
     mk = gpu.heat2d_system if len(shape) == 2 else gpu.heat3d_system
     ivp = mk(n, t_final=1.0, u0=u)
-    G = gpu.backward_euler_propagator(ivp, dT, 1)
+    G = gpu.backward_euler_propagator(ivp, steps * dT, steps, solver=solver)
     got = G.apply(u)
-    want = H.ImplicitND(shape, h, dT, direct=True).apply(u)
-    assert rel_l2(got, want) < 1e-11
-    G32 = gpu.backward_euler_propagator(ivp, dT, 1, dtype="float32", cg_rtol=1e-6)
+    want = u
+    for _ in range(steps):
+        want = H.ImplicitND(shape, h, dT, direct=True).apply(want)
+    assert rel_l2(got, want) < tol, rel_l2(got, want)
+    G32 = gpu.backward_euler_propagator(ivp, steps * dT, steps, dtype="float32", cg_rtol=1e-6, solver=solver)
     assert rel_l2(G32.apply(u), want) < 1e-5
-    # deterministic: same input bits -> same output bits
+    # deterministic: same input bits -> same output bits; batch == single
     assert np.array_equal(G.apply(u), got)
+    import torch
+    xs = torch.tensor(np.stack([u, -2 * u]), device="cuda", dtype=torch.float64)
+    out = G.apply_batch(xs)
+    assert torch.equal(out[0], G.apply(xs[0]))
+
+
+@pytest.mark.parametrize("shape,dtype,tol", [((1024, 1024), "float64", 4e-15), ((1024, 1024), "float32", 2e-6),
+                                             ((256, 256, 256), "float32", 2e-6), ((128, 128, 128), "float64", 4e-15)])
+def test_direct_coarse_residual_at_config_size(gpu, shape, dtype, tol):
+    """Size-independent check at the C3/C4 shapes: the normwise backward
+    error ||b - A x|| / (||A|| ||x|| + ||b||) of A x = b, A = I - dT Lap_h
+    (||A||_2 < 1 + 4 d c), evaluated in fp64 on the device. A backward-stable
+    solve keeps it at a small multiple of the working precision."""
+    import torch
+    n = shape[0]
+    h = 1.0 / (n + 1)
+    dT = (100 if len(shape) == 2 else 30) * h * h
+    u = H.sine_u0_nd(shape, H.modes_2d() if len(shape) == 2 else H.modes_3d(), 0).reshape(-1)
+    u = u + 1e-3 * np.random.default_rng(3).standard_normal(u.size)
+    mk = gpu.heat2d_system if len(shape) == 2 else gpu.heat3d_system
+    ivp = mk(n, t_final=1.0, u0=u)
+    G = gpu.backward_euler_propagator(ivp, dT, 1, dtype=dtype)
+    b = torch.tensor(u, device="cuda", dtype=G.dtype)
+    x = G.apply_batch(b.reshape(1, -1))[0].double().reshape(shape)
+    bd = b.double().reshape(shape)
+    c = dT / (h * h)
+    lap = -2 * len(shape) * x
+    for ax in range(len(shape)):
+        lap = lap + torch.roll(x, 1, ax) + torch.roll(x, -1, ax)
+        # zero Dirichlet: undo the wrap-around
+        idx0 = [slice(None)] * len(shape)
+        idx0[ax] = 0
+        idxl = [slice(None)] * len(shape)
+        idxl[ax] = n - 1
+        lap[tuple(idx0)] -= x[tuple(idxl)]
+        lap[tuple(idxl)] -= x[tuple(idx0)]
+    anorm = 1 + 4 * len(shape) * c
+    res = (x - c * lap - bd).norm() / (anorm * x.norm() + bd.norm())
+    print(f"backward error {shape} {dtype}: {res.item():.3e}")
+    assert res.item() < tol, res.item()
 
 
 def test_cg_reports_nonconvergence(gpu):
     n = 32
     ivp = gpu.heat2d_system(n, t_final=1.0, u0=np.ones(n * n))
-    G = gpu.backward_euler_propagator(ivp, 1.0, 1, cg_rtol=1e-14, cg_maxit=3)
+    G = gpu.backward_euler_propagator(ivp, 1.0, 1, cg_rtol=1e-14, cg_maxit=3, solver="cg")
     with pytest.raises(gpu.ConvergenceFailure) as err:
         G.apply(np.ones(n * n))
     assert err.value.estimate > 0
+
+
+def test_unknown_nd_solver_rejected(gpu):
+    ivp = gpu.heat2d_system(8, t_final=1.0, u0=np.ones(64))
+    with pytest.raises(ValueError):
+        gpu.backward_euler_propagator(ivp, 0.1, 1, solver="lu")
