@@ -96,7 +96,8 @@ struct pint_op {
   int64_t cg_nblocks = 0;
   int64_t cg_last_iters = 0;
   void *spec_q = nullptr;      // direct solve: n x n sine transform (T)
-  double *spec_mu = nullptr;   // direct solve: 1-D Laplacian eigenvalues * h^2
+  void *spec_ip = nullptr;     // direct solve: reciprocal pivots [J][mode] (T)
+  int spec_J = 0;
 };
 
 // 1-D launchers (tri1d.cu)

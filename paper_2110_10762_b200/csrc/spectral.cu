@@ -12,8 +12,8 @@
 //   2-D [y][x]:    W = B Q ;  tridiag_y(1 + 2c + c mu_kx, -c) ;  X = W Q
 //   3-D [z][y][x]: W = B Q ;  W_z = Q W_z ;  tridiag_z(1 + 2c + c (mu_kx + mu_ky), -c) ;
 //                  W_z = Q W_z ;  X = W Q
-// with c = dT / h^2. The transforms are dense GEMMs with an n x n operand
-// (2 n FLOP per point per transformed axis, FP64/FP32 SIMT tiles; the
+// with c = dT / h^2. The transforms are dense GEMMs, halved by the parity
+// symmetry of Q (n FLOP per point per transformed axis, FP64/FP32 SIMT tiles; the
 // tensor cores have no FP64 mode worth using on sm_100 and TF32 would not
 // hold the fp32 tolerance), the tridiagonal sweeps are one thread per mode
 // (coalesced across modes). Exact to rounding: no iteration, no tolerance,
@@ -28,6 +28,14 @@
 
 namespace {
 
+// C = A B, row-major, batched (z -> (z / inner, z % inner) with per-operand
+// strides). FOLD applies the parity symmetry of the sine transform,
+// Q[n-1-i][j] = (-1)^j Q[i][j], to halve the K extent: z = 2*batch + par and
+//   FOLD 1 (transform along A's columns): A'[m][k] = A[m][k] +- A[m][n-1-k],
+//          B = half[par] (K' x N_par), output column 2 q + par;
+//   FOLD 2 (transform along B's rows):    B'[k][x] = B[k][x] +- B[n-1-k][x],
+//          A = half[par] (M_par x K'), output row 2 q + par;
+// with K' = ceil(n/2) and the sign + for even, - for odd output indices.
 template <typename T>
 struct GemmArgs {
   const T *A;
@@ -35,8 +43,12 @@ struct GemmArgs {
   T *C;
   int M, N, K;
   int lda, ldb, ldc;
-  int inner;  // batch index z -> (z / inner, z % inner)
+  int inner;
   int64_t a_outer, a_inner, b_outer, b_inner, c_outer, c_inner;
+  const T *half[2];
+  int mn[2];
+  int ldh[2];
+  int nfold;
 };
 
 __device__ __forceinline__ void ld2(const float *p, float *d) {
@@ -66,22 +78,33 @@ __device__ __forceinline__ void ldv(const T *p, T *d) {
   else ld4(p, d);
 }
 
-// C = A B (row-major, batched). 256 threads as 16 x 16; each thread owns a
-// TM x TN register tile split in two halves per axis (rows ty*HM.. and
-// BM/2 + ty*HM..), so its shared-memory operand reads are 2 vector loads per
-// axis. K staged 8 at a time, double buffered through registers.
-template <typename T, int BM, int BN>
-__global__ void __launch_bounds__(256) gemm_nn(const GemmArgs<T> g) {
+// 256 threads as 16 x 16; each thread owns a TM x TN register tile split in
+// two halves per axis (rows ty*HM.. and BM/2 + ty*HM..), so its shared-memory
+// operand reads are 2 vector loads per axis. K staged 8 at a time, double
+// buffered through registers.
+template <typename T, int BM, int BN, int FOLD, int MINB>
+__global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
   constexpr int BK = 8, TM = BM / 16, TN = BN / 16, HM = TM / 2, HN = TN / 2;
   constexpr int LA = BM * BK / 256, LB = BN * BK / 256;
   __shared__ __align__(16) T As[2][BK][BM];
   __shared__ __align__(16) T Bs[2][BK][BN];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int bo = blockIdx.z / g.inner, bi = blockIdx.z % g.inner;
-  const T *A = g.A + bo * g.a_outer + bi * g.a_inner;
-  const T *B = g.B + bo * g.b_outer + bi * g.b_inner;
+  int z = blockIdx.z, par = 0;
+  if (FOLD) {
+    par = z & 1;
+    z >>= 1;
+  }
+  const int bo = z / g.inner, bi = z % g.inner;
+  const T *A = FOLD == 2 ? g.half[par] : g.A + bo * g.a_outer + bi * g.a_inner;
+  const T *B = FOLD == 1 ? g.half[par] : g.B + bo * g.b_outer + bi * g.b_inner;
+  const int lda = FOLD == 2 ? g.ldh[par] : g.lda;
+  const int ldb = FOLD == 1 ? g.ldh[par] : g.ldb;
+  const int M = FOLD == 2 ? g.mn[par] : g.M;
+  const int N = FOLD == 1 ? g.mn[par] : g.N;
+  const int K = g.K;
   T *C = g.C + bo * g.c_outer + bi * g.c_inner;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M || n0 >= N) return;
   const int a_row = tid / (BK / LA), a_k = (tid % (BK / LA)) * LA;
   const int b_row = tid / (BN / LB), b_n = (tid % (BN / LB)) * LB;
   T ra[LA], rb[LB];
@@ -89,12 +112,28 @@ __global__ void __launch_bounds__(256) gemm_nn(const GemmArgs<T> g) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const int m = m0 + a_row, k = k0 + a_k + i;
-      ra[i] = (m < g.M && k < g.K) ? A[(int64_t)m * g.lda + k] : T(0);
+      T v = T(0);
+      if (m < M && k < K) {
+        v = A[(int64_t)m * lda + k];
+        if (FOLD == 1) {
+          const int k2 = g.nfold - 1 - k;
+          if (k2 > k) v = par ? v - A[(int64_t)m * lda + k2] : v + A[(int64_t)m * lda + k2];
+        }
+      }
+      ra[i] = v;
     }
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
       const int k = k0 + b_row, n = n0 + b_n + i;
-      rb[i] = (k < g.K && n < g.N) ? B[(int64_t)k * g.ldb + n] : T(0);
+      T v = T(0);
+      if (k < K && n < N) {
+        v = B[(int64_t)k * ldb + n];
+        if (FOLD == 2) {
+          const int k2 = g.nfold - 1 - k;
+          if (k2 > k) v = par ? v - B[(int64_t)k2 * ldb + n] : v + B[(int64_t)k2 * ldb + n];
+        }
+      }
+      rb[i] = v;
     }
   };
   auto store = [&](int buf) {
@@ -111,7 +150,7 @@ __global__ void __launch_bounds__(256) gemm_nn(const GemmArgs<T> g) {
   load(0);
   store(0);
   __syncthreads();
-  const int nk = (g.K + BK - 1) / BK;
+  const int nk = (K + BK - 1) / BK;
   for (int t = 0; t < nk; ++t) {
     const int buf = t & 1;
     if (t + 1 < nk) load((t + 1) * BK);
@@ -133,65 +172,109 @@ __global__ void __launch_bounds__(256) gemm_nn(const GemmArgs<T> g) {
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + (i < HM ? ty * HM + i : BM / 2 + ty * HM + (i - HM));
-    if (m >= g.M) continue;
+    if (m >= M) continue;
+    const int64_t row = FOLD == 2 ? 2 * m + par : m;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + (j < HN ? tx * HN + j : BN / 2 + tx * HN + (j - HN));
-      if (n < g.N) C[(int64_t)m * g.ldc + n] = acc[i][j];
+      if (n < N) C[row * g.ldc + (FOLD == 1 ? 2 * n + par : n)] = acc[i][j];
     }
   }
 }
 
-template <typename T>
+template <typename T, int FOLD>
 void gemm(const GemmArgs<T> &g, int batch, cudaStream_t s) {
-  auto tiles = [&](int bm, int bn) {
-    return (int64_t)((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn) * batch;
-  };
+  const int M = FOLD == 2 ? g.mn[0] : g.M, N = FOLD == 1 ? g.mn[0] : g.N;  // parity 0 is the larger half
+  const int zs = batch * (FOLD ? 2 : 1);
+  auto tiles = [&](int bm, int bn) { return (int64_t)((M + bm - 1) / bm) * ((N + bn - 1) / bn) * zs; };
   // FP64: 4x4 per thread already keeps the DFMA pipe ahead of shared memory.
-  // FP32: 8x8 per thread when that still fills two waves of 148 SMs.
-  const bool big = sizeof(T) == 4 && tiles(128, 128) >= 2 * 148;
-  if (big) {
-    dim3 grid((unsigned)((g.N + 127) / 128), (unsigned)((g.M + 127) / 128), (unsigned)batch);
-    gemm_nn<T, 128, 128><<<grid, 256, 0, s>>>(g);
-  } else {
-    dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64), (unsigned)batch);
-    gemm_nn<T, 64, 64><<<grid, 256, 0, s>>>(g);
+  // FP32: 8x8 per thread (two CTAs per SM) when that still fills two waves.
+  if constexpr (sizeof(T) == 4) {
+    if (tiles(128, 128) >= 2 * 148) {
+      dim3 grid((unsigned)((N + 127) / 128), (unsigned)((M + 127) / 128), (unsigned)zs);
+      gemm_nn<T, 128, 128, FOLD, 2><<<grid, 256, 0, s>>>(g);
+      PINT_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  {
+    dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)zs);
+    gemm_nn<T, 64, 64, FOLD, 1><<<grid, 256, 0, s>>>(g);
   }
   PINT_CUDA(cudaGetLastError());
 }
 
 // One thread per transverse mode: `steps` backward-Euler solves along the
 // slowest axis (n points, `nsys` modes interleaved: point j of mode i at
-// u[j * nsys + i]). Pivots in FP64, recomputed per step (c/p_j kept in
-// `ratio` for the back substitution).
+// u[j * nsys + i]). The reciprocal pivots 1/p_j (p_0 = d, p_j = d - c^2 /
+// p_{j-1}) do not depend on the right-hand side and converge geometrically
+// in j, so they come from a host-built table ipt[j][mode] (long double,
+// rows j < J; row J-1 is the converged value used for every j >= J-1). The
+// dependent chain is then one FMA and one multiply per point; loads are
+// issued a block of U points ahead of it.
 template <typename T>
-__global__ void __launch_bounds__(256)
-modal_tridiag(T *__restrict__ u, T *__restrict__ ratio, const double *__restrict__ mu, int n, int64_t nsys,
-              int two_axes, double c, int64_t steps) {
+__global__ void __launch_bounds__(128)
+modal_tridiag(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_t nsys, double c, int64_t steps) {
+  constexpr int U = 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsys) return;
-  double m = mu[i % n];
-  if (two_axes) m += mu[i / n];
-  const double d = 1.0 + 2.0 * c + c * m;
+  const double ipinf = (double)ipt[(int64_t)(J - 1) * nsys + i];
+  auto ipat = [&](int j) { return j < J ? (double)ipt[(int64_t)j * nsys + i] : ipinf; };
   for (int64_t s = 0; s < steps; ++s) {
-    double ip = 1.0 / d;
-    double g = (double)u[i] * ip;
-    double r = c * ip;
-    u[i] = (T)g;
-    ratio[i] = (T)r;
-    for (int j = 1; j < n; ++j) {
-      const int64_t o = (int64_t)j * nsys + i;
-      ip = 1.0 / (d - c * r);
-      g = ((double)u[o] + c * g) * ip;
-      r = c * ip;
-      u[o] = (T)g;
-      ratio[o] = (T)r;
+    double g = 0.0;
+    T cur[U], nxt[U];
+    double cip[U], nip[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      cur[q] = q < n ? u[(int64_t)q * nsys + i] : T(0);
+      cip[q] = ipat(q);
     }
+    for (int j0 = 0; j0 < n; j0 += U) {
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        nxt[q] = j0 + U + q < n ? u[(int64_t)(j0 + U + q) * nsys + i] : T(0);
+        nip[q] = ipat(j0 + U + q);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if (j0 + q < n) {
+          g = fma(c, g, (double)cur[q]) * cip[q];
+          u[(int64_t)(j0 + q) * nsys + i] = (T)g;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        cur[q] = nxt[q];
+        cip[q] = nip[q];
+      }
+    }
+    // back substitution x_j = g_j + (c / p_j) x_{j+1}, blocks of U from the top
     double x = g;
-    for (int j = n - 2; j >= 0; --j) {
-      const int64_t o = (int64_t)j * nsys + i;
-      x = (double)u[o] + (double)ratio[o] * x;
-      u[o] = (T)x;
+    T cg[U], ng[U];
+    auto fetch = [&](int top, T *gg, double *pp) {
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int jj = top - q;
+        gg[q] = jj >= 0 ? u[(int64_t)jj * nsys + i] : T(0);
+        pp[q] = jj >= 0 ? ipat(jj) : 0.0;
+      }
+    };
+    fetch(n - 2, cg, cip);
+    for (int top = n - 2; top >= 0; top -= U) {
+      fetch(top - U, ng, nip);
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int jj = top - q;
+        if (jj >= 0) {
+          x = fma(c * cip[q], x, (double)cg[q]);
+          u[(int64_t)jj * nsys + i] = (T)x;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        cg[q] = ng[q];
+        cip[q] = nip[q];
+      }
     }
   }
 }
@@ -200,31 +283,63 @@ template <typename T>
 void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   const int n = (int)op->nx;
   const int64_t n2 = (int64_t)n * n;
+  const int kh = (n + 1) / 2, n0 = (n + 1) / 2, n1 = n / 2;  // folded K; output counts per parity
   T *w1 = reinterpret_cast<T *>(op->cg_work);
   T *w2 = w1 + op->dim;
-  T *rat = w2 + op->dim;
   const T *Q = reinterpret_cast<const T *>(op->spec_q);
+  // host layout of spec_q: Qh[0] (kh x n0), Qh[1] (kh x n1), QhT[0] (n0 x kh), QhT[1] (n1 x kh)
+  const T *qh0 = Q, *qh1 = qh0 + (size_t)kh * n0, *qt0 = qh1 + (size_t)kh * n1, *qt1 = qt0 + (size_t)n0 * kh;
   const double c = op->dt / (op->desc.h * op->desc.h);
   auto xform_last = [&](const T *src, T *dst, int rows) {  // dst = src Q (rows x n)
-    GemmArgs<T> g{src, Q, dst, rows, n, n, n, n, n, 1, 0, 0, 0, 0, 0, 0};
-    gemm<T>(g, 1, s);
+    GemmArgs<T> g{};
+    g.A = src;
+    g.C = dst;
+    g.M = rows;
+    g.K = kh;
+    g.lda = n;
+    g.ldc = n;
+    g.inner = 1;
+    g.half[0] = qh0;
+    g.half[1] = qh1;
+    g.mn[0] = n0;
+    g.mn[1] = n1;
+    g.ldh[0] = n0;
+    g.ldh[1] = n1 > 0 ? n1 : 1;
+    g.nfold = n;
+    gemm<T, 1>(g, 1, s);
   };
   auto xform_mid = [&](const T *src, T *dst) {  // dst_z = Q src_z for every z plane
-    GemmArgs<T> g{Q, src, dst, n, n, n, n, n, n, n, 0, 0, 0, n2, 0, n2};
-    gemm<T>(g, n, s);
+    GemmArgs<T> g{};
+    g.B = src;
+    g.C = dst;
+    g.N = n;
+    g.K = kh;
+    g.ldb = n;
+    g.ldc = n;
+    g.inner = n;
+    g.b_inner = n2;
+    g.c_inner = n2;
+    g.half[0] = qt0;
+    g.half[1] = qt1;
+    g.mn[0] = n0;
+    g.mn[1] = n1;
+    g.ldh[0] = kh;
+    g.ldh[1] = kh;
+    g.nfold = n;
+    gemm<T, 2>(g, n, s);
   };
-  const unsigned threads = 256;
+  const unsigned threads = 128;
   if (op->desc.ndim == 2) {
     xform_last(b, w1, n);
-    modal_tridiag<T><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(w1, rat, op->spec_mu, n, n, 0, c,
-                                                                               op->desc.steps);
+    modal_tridiag<T><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
+        w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
     PINT_CUDA(cudaGetLastError());
     xform_last(w1, x, n);
   } else {
     xform_last(b, w1, (int)n2);
     xform_mid(w1, w2);
-    modal_tridiag<T><<<(unsigned)((n2 + threads - 1) / threads), threads, 0, s>>>(w2, rat, op->spec_mu, n, n2, 1,
-                                                                                c, op->desc.steps);
+    modal_tridiag<T><<<(unsigned)((n2 + threads - 1) / threads), threads, 0, s>>>(
+        w2, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n2, c, op->desc.steps);
     PINT_CUDA(cudaGetLastError());
     xform_mid(w2, w1);
     xform_last(w1, x, (int)n2);
@@ -242,27 +357,75 @@ void spectral_setup(pint_op *op) {
   const size_t esz = op->desc.dtype == PINT_F64 ? 8 : 4;
   op->cg_work_bytes = (size_t)3 * op->dim * esz;
   PINT_CUDA(cudaMalloc(&op->cg_work, op->cg_work_bytes));
-  std::vector<double> mu(n);
-  std::vector<double> qd((size_t)n * n);
-  std::vector<float> qf(esz == 4 ? (size_t)n * n : 0);
+  std::vector<long double> mu(n);
+  std::vector<long double> q((size_t)n * n);
   const long double pi = 3.141592653589793238462643383279502884L;
   const long double scale = sqrtl(2.0L / (long double)(n + 1));
   for (int64_t k = 0; k < n; ++k) {
     const long double sk = sinl(pi * (long double)(k + 1) / (2.0L * (long double)(n + 1)));
-    mu[k] = (double)(4.0L * sk * sk);
+    mu[k] = 4.0L * sk * sk;
   }
   for (int64_t j = 0; j < n; ++j)
     for (int64_t k = 0; k < n; ++k) {
       // reduce (j+1)(k+1) mod 2(n+1) before the sine: exact integer argument
       const int64_t a = ((j + 1) * (k + 1)) % (2 * (n + 1));
       const long double v = scale * sinl(pi * (long double)a / (long double)(n + 1));
-      qd[(size_t)j * n + k] = (double)v;
-      if (esz == 4) qf[(size_t)j * n + k] = (float)v;
+      q[(size_t)j * n + k] = v;
     }
-  PINT_CUDA(cudaMalloc(&op->spec_mu, sizeof(double) * n));
-  PINT_CUDA(cudaMemcpy(op->spec_mu, mu.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-  PINT_CUDA(cudaMalloc(&op->spec_q, esz * n * n));
-  PINT_CUDA(cudaMemcpy(op->spec_q, esz == 8 ? (const void *)qd.data() : (const void *)qf.data(), esz * n * n,
+  // parity-folded halves (see GemmArgs): Qh[par][k][t] = Q[k][2t+par],
+  // QhT[par][t][k] = Q[2t+par][k], k < ceil(n/2)
+  const int64_t kh = (n + 1) / 2, cnt[2] = {(n + 1) / 2, n / 2};
+  std::vector<long double> packed;
+  for (int par = 0; par < 2; ++par)
+    for (int64_t k = 0; k < kh; ++k)
+      for (int64_t t = 0; t < cnt[par]; ++t) packed.push_back(q[(size_t)k * n + 2 * t + par]);
+  for (int par = 0; par < 2; ++par)
+    for (int64_t t = 0; t < cnt[par]; ++t)
+      for (int64_t k = 0; k < kh; ++k) packed.push_back(q[(size_t)(2 * t + par) * n + k]);
+  std::vector<double> qd(packed.size());
+  std::vector<float> qf(esz == 4 ? packed.size() : 0);
+  for (size_t e = 0; e < packed.size(); ++e) {
+    qd[e] = (double)packed[e];
+    if (esz == 4) qf[e] = (float)packed[e];
+  }
+  // reciprocal pivots per transverse mode, rows until every mode has
+  // converged (|p_j - p_{j-1}| <= 2^-64 p_j), capped at n
+  const long double cl = (long double)op->dt / ((long double)op->desc.h * (long double)op->desc.h);
+  const int64_t nsys = op->desc.ndim == 2 ? n : n * n;
+  std::vector<long double> dmode(nsys);
+  for (int64_t m = 0; m < nsys; ++m) {
+    const long double mus = op->desc.ndim == 2 ? mu[m] : mu[m % n] + mu[m / n];
+    dmode[m] = 1.0L + 2.0L * cl + cl * mus;
+  }
+  int64_t J = 1;
+  {
+    // the slowest-converging mode is the one with the smallest diagonal
+    long double dmin = dmode[0];
+    for (int64_t m = 1; m < nsys; ++m) dmin = std::min(dmin, dmode[m]);
+    long double pv = dmin;
+    for (J = 1; J < n; ++J) {
+      const long double pn = dmin - cl * cl / pv;
+      if (fabsl(pn - pv) <= ldexpl(pn, -64)) break;
+      pv = pn;
+    }
+    J = std::min<int64_t>(J + 1, n);
+  }
+  std::vector<double> ipd((size_t)J * nsys);
+  std::vector<float> ipf(esz == 4 ? (size_t)J * nsys : 0);
+  for (int64_t m = 0; m < nsys; ++m) {
+    long double pv = dmode[m];
+    for (int64_t jj = 0; jj < J; ++jj) {
+      if (jj > 0) pv = dmode[m] - cl * cl / pv;
+      ipd[(size_t)jj * nsys + m] = (double)(1.0L / pv);
+      if (esz == 4) ipf[(size_t)jj * nsys + m] = (float)(1.0L / pv);
+    }
+  }
+  op->spec_J = (int)J;
+  PINT_CUDA(cudaMalloc(&op->spec_ip, esz * ipd.size()));
+  PINT_CUDA(cudaMemcpy(op->spec_ip, esz == 8 ? (const void *)ipd.data() : (const void *)ipf.data(),
+                       esz * ipd.size(), cudaMemcpyHostToDevice));
+  PINT_CUDA(cudaMalloc(&op->spec_q, esz * qd.size()));
+  PINT_CUDA(cudaMemcpy(op->spec_q, esz == 8 ? (const void *)qd.data() : (const void *)qf.data(), esz * qd.size(),
                        cudaMemcpyHostToDevice));
 }
 
@@ -278,7 +441,7 @@ void spectral_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch
 
 void spectral_destroy(pint_op *op) {
   if (op->spec_q) cudaFree(op->spec_q);
-  if (op->spec_mu) cudaFree(op->spec_mu);
+  if (op->spec_ip) cudaFree(op->spec_ip);
   op->spec_q = nullptr;
-  op->spec_mu = nullptr;
+  op->spec_ip = nullptr;
 }

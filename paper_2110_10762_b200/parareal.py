@@ -178,7 +178,7 @@ class SyncEngine:
         self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
         self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.fonly = torch.zeros(1, dtype=torch.uint8, device=dev)
+        self.fonly = torch.zeros(p + 1, dtype=torch.bool, device=dev)  # generic sweep: per-slice F-only mask
         self.host = torch.zeros(2, dtype=torch.float64).pin_memory() if torch.cuda.is_available() else None
         self.fused = coarse.is_tridiagonal
         self.prev = self.lam_a
@@ -237,12 +237,15 @@ class SyncEngine:
             nxt[k - 1].copy_(prev[k - 1])
             self.deltas[k - 1] = 0.0
         g = torch.empty(1, self.fine.dim, dtype=self.fine.dtype, device=nxt.device)
+        if not chain_in:
+            self.fonly[k] = True
         for i in range(k, p + 1):
             self.coarse.apply_ptr(nxt[i - 1].data_ptr(), g.data_ptr(), 1, self.fine.dim)
-            f_only = float(self.deltas[i - 1]) == 0.0 if (chain_in or i > k) else True
-            self.fonly.fill_(1 if f_only else 0)
+            if chain_in or i > k:
+                # F-only branch iff slice i-1 did not move (delta 0), decided on the device
+                torch.eq(self.deltas[i - 1:i], 0.0, out=self.fonly[i:i + 1])
             correct_into(self.fine, g, self.fv[i:i + 1], self.gcache[i:i + 1], prev[i:i + 1], nxt[i:i + 1],
-                         self.fonly, self.deltas[i:i + 1], self.flag, 1)
+                         self.fonly[i:i + 1], self.deltas[i:i + 1], self.flag, 1)
             self.gcache[i].copy_(g[0])
 
     def read_delta(self) -> float:
