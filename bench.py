@@ -335,6 +335,10 @@ def run_ours(args, rank: int, world: int) -> None:
 
 
 def time_to_tolerance(coarse, fine, u0, p: int, eps: float = 1e-10) -> dict:
+    """Sync Parareal to eps (wall clock after device sync), the
+    device async runtime to the same eps, both checked against the
+    sequential fine solve on the GPU, plus the reference cost model fed with
+    the measured C_F / C_G."""
     import torch
 
     import paper_2110_10762_b200 as pb
@@ -344,8 +348,26 @@ def time_to_tolerance(coarse, fine, u0, p: int, eps: float = 1e-10) -> dict:
     tr = pb.run_parareal(coarse, fine, u0, p, eps, record_iterates=False)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return {"seconds": wall, "k": tr.k_final, "stop_reason": tr.stop_reason, "epsilon": eps,
-            "last_delta": tr.deltas[-1]}
+    seq = pb.sequential_fine_solve(fine, u0, p).tensor
+
+    def err(x):
+        d = (x - seq).abs().max().item()
+        return {"max_abs_vs_seq_fine": d, "rel_l2_vs_seq_fine": ((x - seq).norm() / seq.norm()).item()}
+
+    out = {"seconds": wall, "k": tr.k_final, "stop_reason": tr.stop_reason, "epsilon": eps,
+           "last_delta": tr.deltas[-1], **err(tr.final.tensor)}
+    kappa = None
+    try:
+        res = pb.run_async_parareal_device(coarse, fine, u0, p, eps)
+        kappa = res.kappa
+        out["async_device"] = {"seconds": res.wall_s, "kappa": res.kappa, "activations": res.activations,
+                               "stop_reason": res.stop_reason, "concurrent_clusters": res.concurrent_clusters,
+                               **err(res.final.tensor)}
+    except Exception as exc:  # reported, never silently replaced
+        out["async_device"] = {"error": f"{type(exc).__name__}: {exc}"}
+    costs = pb.measure_costs(coarse, fine, p)
+    out["cost_model"] = pb.model_report(costs, p, k=tr.k_final, kappa=kappa, measured_sync_s=wall)
+    return out
 
 
 def main():

@@ -39,6 +39,20 @@ from .errors import (
     NativeLibraryError,
     SingularMatrixError,
     SingularSystemError,
+    UndefinedLimitError,
+    UnfittableError,
+)
+from .costmodel import (
+    CostParams,
+    SpeedupReport,
+    async_cost,
+    asymptotic_speedups,
+    fit_overhead,
+    measure_costs,
+    model_report,
+    sequential_cost,
+    speedup_bound,
+    sync_cost,
 )
 from .linalg import BlockVector
 from .model import (
