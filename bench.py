@@ -358,11 +358,12 @@ def time_to_tolerance(coarse, fine, u0, p: int, eps: float = 1e-10) -> dict:
            "last_delta": tr.deltas[-1], **err(tr.final.tensor)}
     kappa = None
     try:
-        res = pb.run_async_parareal_device(coarse, fine, u0, p, eps)
+        res = pb.run_async_parareal_device(coarse, fine, u0, p, eps, record_trace=True)
         kappa = res.kappa
         out["async_device"] = {"seconds": res.wall_s, "kappa": res.kappa, "activations": res.activations,
                                "stop_reason": res.stop_reason, "concurrent_clusters": res.concurrent_clusters,
-                               **err(res.final.tensor)}
+                               **err(res.final.tensor),
+                               "audit": pb.audit_device_trace(res.trace_records, p, res.per_component_counts)}
     except Exception as exc:  # reported, never silently replaced
         out["async_device"] = {"error": f"{type(exc).__name__}: {exc}"}
     costs = pb.measure_costs(coarse, fine, p)

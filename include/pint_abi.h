@@ -24,6 +24,8 @@
  *   pint_async_run          <- run_async_parareal           async_parareal.py:61-84
  *                              (real concurrency instead of the
  *                               simulate_async event loop, async_engine.py:238-365)
+ *   pint_async_run_traced   <- + AsyncTrace / UpdateRecord  async_engine.py:122-190
+ *                              (audited as validate_schedule, async_engine.py:402-459)
  *
  * Error codes map onto the reference's exception taxonomy (errors.py):
  *   PINT_EDIM       -> DimensionError                errors.py:10-11
@@ -221,6 +223,21 @@ int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p,
                    double epsilon, int64_t max_events, double delay_frac,
                    uint64_t seed, void *final_out, int64_t *counts_out,
                    int64_t *info_out, void *stream);
+
+/*
+ * pint_async_run plus a per-activation trace (the device
+ * analogue of the reference's UpdateRecord list, async_engine.py:122-131,
+ * audited like validate_schedule, async_engine.py:402-459). trace_out (host)
+ * receives min(activations, trace_cap) records of 8 int64 in publish order:
+ * {slice i, fresh version of slice i-1 read, remembered version, F-only flag,
+ *  delta (IEEE-754 bits), globaltimer ns at F start, globaltimer ns at
+ *  publish, cluster id}. Versions count publishes per slice (0 = initial).
+ */
+int pint_async_run_traced(pint_op *fine, pint_op *coarse, const void *lam0,
+                          int64_t p, double epsilon, int64_t max_events,
+                          double delay_frac, uint64_t seed, void *final_out,
+                          int64_t *counts_out, int64_t *info_out,
+                          int64_t *trace_out, int64_t trace_cap, void *stream);
 
 /* max over deltas_dev[lo..hi) -> *out_dev (device double), deterministic. */
 int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,

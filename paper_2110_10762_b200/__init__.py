@@ -27,6 +27,7 @@ from .async_parareal import (
     run_async_parareal,
     simulate_parareal_async,
     run_async_parareal_device,
+    audit_device_trace,
     DeviceAsyncResult,
 )
 from .errors import (

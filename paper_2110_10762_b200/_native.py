@@ -77,6 +77,8 @@ SIGNATURES = {
                                       c_void_p, c_void_p, c_void_p]),
     "pint_async_run": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_double, c_i64, c_double, ctypes.c_uint64,
                                c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pint_async_run_traced": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_double, c_i64, c_double,
+                                      ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p]),
     "pint_max_reduce": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "pint_equal_flag": (c_int, [c_void_p, c_i32, c_i64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pint_tri1d_plan_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p, c_void_p, c_void_p]),

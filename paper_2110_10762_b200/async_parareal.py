@@ -25,6 +25,7 @@ from . import _device, _native
 from .async_engine import (
     STOP_PREDICATE,
     STOP_QUIESCENCE,
+    POLICY_ROUND_ROBIN,
     AsyncSchedule,
     AsyncTrace,
     EngineView,
@@ -178,10 +179,16 @@ def run_async_parareal(coarse, fine, u0, p: int, schedule: AsyncSchedule, epsilo
     return simulate_parareal_async(coarse, fine, init, schedule, stop=stop, record_snapshots=record_snapshots)
 
 
-class DeviceAsyncResult:
-    """Outcome of ``run_async_parareal_device``."""
+TRACE_FIELDS = ("slice", "fresh_version", "remembered_version", "f_only", "delta_bits", "t_start_ns",
+                "t_publish_ns", "cluster")
 
-    def __init__(self, final, counts, info, wall_s):
+
+class DeviceAsyncResult:
+    """Outcome of ``run_async_parareal_device``. With ``record_trace=True``
+    ``trace_records`` holds one int64 row per published activation, in
+    publish order (columns ``TRACE_FIELDS``)."""
+
+    def __init__(self, final, counts, info, wall_s, trace_records=None, p=None, seed=0):
         self.final = final
         self.per_component_counts = counts
         self.activations = int(info[0])
@@ -189,16 +196,84 @@ class DeviceAsyncResult:
         self.retries = int(info[3])
         self.concurrent_clusters = int(info[4])
         self.wall_s = wall_s
+        self.trace_records = trace_records
+        self.p = p
+        self.seed = seed
 
     @property
     def kappa(self) -> int:
         """Busiest worker's activation count (the paper's kappa(k~))."""
         return int(np.max(self.per_component_counts[1:])) if len(self.per_component_counts) > 1 else 0
 
+    def to_async_trace(self) -> AsyncTrace:
+        """The device run as the reference's trace type (async_engine.py:122-190):
+        event k = k-th publish; component i read (i-1, FRESH, v) and
+        (i-1, REMEMBERED, v_rem). Values are not snapshotted (digest "")."""
+        if self.trace_records is None:
+            raise ValueError("run with record_trace=True to get a trace")
+        return device_records_to_trace(self.trace_records, self.p, self.per_component_counts, self.final,
+                                       self.stop_reason, self.seed)
+
+
+def device_records_to_trace(records: np.ndarray, p: int, counts, final, stop_reason: str, seed: int = 0):
+    events = []
+    for k, r in enumerate(np.asarray(records, dtype=np.int64)):
+        i, vf, vr, fonly, dbits = int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4])
+        delta = float(np.array([dbits], dtype=np.int64).view(np.float64)[0])
+        events.append(UpdateRecord(k_global=k, component=i,
+                                   reads=((i - 1, FRESH_SLOT, vf), (i - 1, REMEMBERED_SLOT, vr)),
+                                   digest="", delta=delta, frozen=False))
+    # the device ticket queue claims slices in round-robin order; staleness is whatever the hardware produced
+    sched = AsyncSchedule(seed=int(seed), delay_bound=max(1, len(events)), policy=POLICY_ROUND_ROBIN,
+                          max_events=max(1, len(events)))
+    return AsyncTrace(events=events, snapshots=[], initial=None, per_component_counts=np.asarray(counts),
+                      stop_event=len(events) - 1, stop_reason=stop_reason, schedule=sched, n_updatable=p,
+                      persistent_slots=dict(PERSISTENT_SLOTS), final=final)
+
+
+def audit_device_trace(records: np.ndarray, p: int, counts=None) -> dict:
+    """Race audit of a device async run: replays the publish
+    order through ``validate_schedule`` with an unbounded delay (so only a
+    read of a not-yet-published version counts as a staleness violation —
+    causality) and checks remembered-slot provenance; reports the observed
+    staleness (versions behind the newest at publish time), the per-slice
+    publish counts against ``counts``, and the peak number of activations in
+    flight at once (from the globaltimer stamps)."""
+    from .async_engine import validate_schedule
+
+    rec = np.asarray(records, dtype=np.int64).reshape(-1, len(TRACE_FIELDS))
+    n = len(rec)
+    trace = device_records_to_trace(rec, p, counts if counts is not None else np.zeros(p + 1), None, "")
+    val = validate_schedule(trace, delay_bound=n + 1, window=n + 1)
+    versions = np.zeros(p + 1, dtype=np.int64)
+    stale = []
+    for r in rec:
+        i, vf = int(r[0]), int(r[1])
+        stale.append(int(versions[i - 1] - vf) if i > 1 else 0)
+        versions[i] += 1
+    pub = np.bincount(rec[:, 0], minlength=p + 1) if n else np.zeros(p + 1, dtype=np.int64)
+    # peak concurrency: sweep over [t_start, t_publish] intervals
+    ev = sorted([(int(t0), 1) for t0 in rec[:, 5]] + [(int(t1), -1) for t1 in rec[:, 6]],
+                key=lambda e: (e[0], e[1]))
+    cur = peak = 0
+    for _, d in ev:
+        cur += d
+        peak = max(peak, cur)
+    out = {"events": n, "causality_violations": len(val.staleness_violations),
+           "provenance_violations": len(val.provenance_violations), "max_staleness": int(max(stale, default=0)),
+           "mean_staleness": float(np.mean(stale)) if stale else 0.0, "peak_in_flight": int(peak),
+           "clusters_used": int(len(np.unique(rec[:, 7]))) if n else 0}
+    if counts is not None:
+        out["counts_match"] = bool(np.array_equal(pub[1:], np.asarray(counts)[1:]))
+    out["ok"] = (out["causality_violations"] == 0 and out["provenance_violations"] == 0
+                 and out.get("counts_match", True))
+    return out
+
 
 def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = None, *,
                               max_events: int = 200_000, delay_frac: float = 0.0,
-                              seed: int = 0) -> DeviceAsyncResult:
+                              seed: int = 0, record_trace: bool = False,
+                              trace_cap: int | None = None) -> DeviceAsyncResult:
     """Asynchronous Parareal with real concurrency on the GPU (PAPER.md
     Algorithm 2): one persistent launch; thread-block clusters act as workers
     that claim slice activations, read the freshest published predecessor
@@ -222,16 +297,23 @@ def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = 
     lib = _native.load_library()
     torch.cuda.synchronize(fine.device)
     t0 = time.perf_counter()
-    rc = lib.pint_async_run(fine.handle, coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
-                            float(-1.0 if epsilon is None else epsilon), int(max_events), float(delay_frac),
-                            int(seed), ctypes.c_void_p(out.data_ptr()), counts.ctypes.data_as(ctypes.c_void_p),
-                            info.ctypes.data_as(ctypes.c_void_p),
-                            ctypes.c_void_p(_device.stream_ptr(fine.device)))
+    cap = 0
+    trace_buf = None
+    if record_trace:
+        cap = int(trace_cap if trace_cap is not None else min(max_events, 1_000_000))
+        trace_buf = np.zeros((cap, len(TRACE_FIELDS)), dtype=np.int64)
+    rc = lib.pint_async_run_traced(fine.handle, coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
+                                   float(-1.0 if epsilon is None else epsilon), int(max_events), float(delay_frac),
+                                   int(seed), ctypes.c_void_p(out.data_ptr()), counts.ctypes.data_as(ctypes.c_void_p),
+                                   info.ctypes.data_as(ctypes.c_void_p),
+                                   ctypes.c_void_p(trace_buf.ctypes.data if trace_buf is not None else 0), cap,
+                                   ctypes.c_void_p(_device.stream_ptr(fine.device)))
     _native.check(rc, fine._ctx.handle, "pint_async_run")
     wall = time.perf_counter() - t0
     if info[2]:
         raise ValueError("block entries must be finite")
-    res = DeviceAsyncResult(BlockVector(out, check_finite=False), counts, info, wall)
+    records = trace_buf[:min(int(info[0]), cap)] if trace_buf is not None else None
+    res = DeviceAsyncResult(BlockVector(out, check_finite=False), counts, info, wall, records, p, seed)
     if res.stop_reason == "max_events":
         raise HorizonExhausted(f"no stop condition met within {max_events} activations", res)
     return res

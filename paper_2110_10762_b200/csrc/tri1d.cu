@@ -1070,7 +1070,13 @@ struct AsyncArgs {
   int64_t max_events;
   double delay_frac;       // injected delay per activation: U(0, delay_frac) * t_F
   unsigned long long seed;
+  long long *trace;        // optional: ASYNC_TRACE_FIELDS int64 per published activation, in publish order
+  long long trace_cap;
 };
+
+// trace record: slice, fresh predecessor version read, remembered version,
+// F-only flag, delta (bits), globaltimer at F start / at publish, cluster
+constexpr int ASYNC_TRACE_FIELDS = 8;
 
 __device__ __forceinline__ long long ld_acquire_s64(const long long *p) {
   long long v;
@@ -1286,6 +1292,17 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
       A.stable[i] = fonly ? 1 : 0;
       A.counts[i] += 1;
       const long long ev = (long long)atomicAdd((unsigned long long *)A.events, 1ull) + 1;
+      if (A.trace && ev - 1 < A.trace_cap) {
+        long long *r = A.trace + (ev - 1) * ASYNC_TRACE_FIELDS;
+        r[0] = i;
+        r[1] = v;
+        r[2] = vr;
+        r[3] = fonly ? 1 : 0;
+        r[4] = __double_as_longlong(d);
+        r[5] = (long long)tf0;
+        r[6] = (long long)globaltimer();
+        r[7] = cid;
+      }
       __threadfence();
       st_release_s64(A.ver + i, vi + 1);
       atomicExch(A.busy + i, 0);
@@ -1297,9 +1314,10 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
   cluster.sync();
 }
 
-extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
-                              int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
-                              int64_t *counts_out, int64_t *info_out, void *stream) {
+extern "C" int pint_async_run_traced(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
+                                     int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
+                                     int64_t *counts_out, int64_t *info_out, int64_t *trace_out, int64_t trace_cap,
+                                     void *stream) {
   if (!fine || !coarse) return PINT_EARG;
   pint_ctx *ctx = fine->ctx;
   try {
@@ -1310,6 +1328,7 @@ extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, 
     if (pf.N != pg.N || pf.CH != pg.CH || pf.T != pg.T)
       pint_throw(PINT_EUNSUPPORTED, "fine and coarse operators must share the register layout (same rule family)");
     if (p < 1 || !lam0 || !final_out) pint_throw(PINT_EARG, "bad arguments");
+    if (trace_cap < 0 || (trace_cap > 0 && !trace_out)) pint_throw(PINT_EARG, "trace buffer missing");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t N = pf.N;
     const int R = 3;
@@ -1324,7 +1343,8 @@ extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, 
                  o_gremb = take(sizeof(double) * (p + 1) * N), o_scr = take(sizeof(double) * ncl * 2 * N),
                  o_ver = take(8 * (p + 1)), o_vrem = take(8 * (p + 1)), o_cons = take(8 * (p + 1)),
                  o_busy = take(4 * (p + 1)), o_stab = take(4 * (p + 1)), o_cnt = take(8 * (p + 1)),
-                 o_ld = take(8 * (p + 1)), o_misc = take(64);
+                 o_ld = take(8 * (p + 1)), o_misc = take(64),
+                 o_trace = take(sizeof(long long) * ASYNC_TRACE_FIELDS * (size_t)trace_cap);
     char *w = nullptr;
     PINT_CUDA(cudaMallocAsync((void **)&w, bytes, s));
     PINT_CUDA(cudaMemsetAsync(w + o_ver, 0, o_misc + 64 - o_ver, s));
@@ -1352,6 +1372,8 @@ extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, 
     A.max_events = max_events > 0 ? max_events : 20000;
     A.delay_frac = delay_frac;
     A.seed = seed;
+    A.trace = trace_cap > 0 ? (long long *)(w + o_trace) : nullptr;
+    A.trace_cap = trace_cap;
     // initial versions: ring[i][0] = lam0[i]; remembered = lam0[i-1] (version 0);
     // G(remembered) = G(lam0[i-1]) = lam0[i] (coarse initial iterate)
     const double *L = (const double *)lam0;
@@ -1404,6 +1426,11 @@ extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, 
     PINT_CUDA(cudaMemcpyAsync(flags, A.stop, 8, cudaMemcpyDeviceToHost, s));
     PINT_CUDA(cudaMemcpyAsync(misc, A.events, 16, cudaMemcpyDeviceToHost, s));
     PINT_CUDA(cudaStreamSynchronize(s));
+    if (trace_cap > 0) {
+      const size_t nrec = (size_t)std::min<long long>(misc[0], trace_cap);
+      PINT_CUDA(cudaMemcpyAsync(trace_out, A.trace, sizeof(long long) * ASYNC_TRACE_FIELDS * nrec,
+                                cudaMemcpyDeviceToHost, s));
+    }
     for (int64_t i = 0; i <= p; ++i)
       PINT_CUDA(cudaMemcpyAsync((double *)final_out + i * N, A.ring + ((size_t)i * R + (size_t)(ver[i] % R)) * N,
                                 sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
@@ -1424,4 +1451,11 @@ extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, 
     ctx->last_value = e.value;
     return e.code;
   }
+}
+
+extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
+                              int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
+                              int64_t *counts_out, int64_t *info_out, void *stream) {
+  return pint_async_run_traced(fine, coarse, lam0, p, epsilon, max_events, delay_frac, seed, final_out, counts_out,
+                               info_out, nullptr, 0, stream);
 }

@@ -134,3 +134,36 @@ def test_device_async_fixture_with_boundary_forcing(gpu):
         seq = gpu.sequential_fine_solve(fine, ivp.u0, p).data
         res = gpu.run_async_parareal_device(coarse, fine, ivp.u0, p, None, seed=p)
         assert np.array_equal(res.final.data, seq)
+
+
+@pytest.mark.parametrize("delay,n,p", [(0.0, 1024, 16), (0.3, 1024, 16), (0.0, 65536, 24)])
+def test_device_async_trace_audit(gpu, delay, n, p):
+    """Race audit of real concurrent runs: every published
+    activation read a version that had been published (causality), its
+    remembered reading is the previous fresh reading of the same slice
+    (provenance), per-slice publish counts match the counters, several
+    activations were in flight at once, and the trace exports as the
+    reference's AsyncTrace/JSONL."""
+    from oracle import heat_oracle as H
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 100)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, delay_frac=delay, seed=3, record_trace=True)
+    assert res.stop_reason == "converged"
+    rec = res.trace_records
+    assert len(rec) == res.activations
+    audit = gpu.audit_device_trace(rec, p, res.per_component_counts)
+    assert audit["ok"], audit
+    assert audit["peak_in_flight"] >= 2, audit
+    assert audit["clusters_used"] >= 2, audit
+    # exact quiescence: each slice's last publish was F-only on the newest predecessor
+    last = {}
+    for r in rec:
+        last[int(r[0])] = r
+    assert all(int(last[i][3]) == 1 for i in range(1, p + 1))
+    tr = res.to_async_trace()
+    assert len(tr.events) == res.activations
+    assert tr.to_jsonl().count("\n") == res.activations
+    _, kappa = gpu.update_counts(tr)
+    assert kappa == res.kappa
