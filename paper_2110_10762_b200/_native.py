@@ -14,7 +14,8 @@ import threading
 from . import errors
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libpint_b200.so")
+# PINT_LIB_PATH selects an alternative build (e.g. the phase-timing debug library)
+LIB_PATH = os.environ.get("PINT_LIB_PATH") or os.path.join(PKG, "libpint_b200.so")
 
 PINT_OK = 0
 PINT_EDIM = 1

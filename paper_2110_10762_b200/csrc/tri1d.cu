@@ -413,6 +413,18 @@ __device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t s
 
 #define TAB(f) lds_free(tab + (uint32_t)(f) * 8u)
 
+#ifdef PINT_PHASE_TIMING
+// debug build only (scripts/phase_timing.py): clock64 stamps of one step per warp
+__device__ long long *g_phase_buf;
+__device__ int g_phase_step;
+#define PHASE(id)                                                                                         \
+  if (g_phase_buf && sc == (uint32_t)g_phase_step && (c.lane == 0)) {                                    \
+    g_phase_buf[((size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))) * 8 + (id)] = clock64(); \
+  }
+#else
+#define PHASE(id)
+#endif
+
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -432,6 +444,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
                                          uint32_t sc, double extra_in, double *extra_out) {
   const bool regular = !GENERAL || c.t < P.tb;
   const uint32_t tab = opaque(c.tab);
+  PHASE(0)
   double xo[CN ? CH : 1];
   if (CN) {
 #pragma unroll
@@ -456,6 +469,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     if (regular) y0 = chunk_forward_scaled<CH>(x, P.reg);
     else y0 = chunk_forward_scaled<CH>(x, P.tail);
   }
+  PHASE(1)
   const double ylast = x[CH - 2];
   const double dsep = x[CH - 1];
   double y0n = shfl_down_d(y0, 1);
@@ -468,13 +482,16 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     const double bp = shfl_down_d(b, d);
     b = fma(-TAB(TF_PCR_G + r), bp, fma(-TAB(TF_PCR_A + r), bm, b));
   }
+  PHASE(2)
   const double y1 = b * TAB(TF_PCR_INV);
   const double y1_30 = shfl_d(y1, 30);
   const double pw = fma(-TAB(TF_CP), y1_30, b);
   const double gP = shfl_d(pw, 31);
   const double gQ = shfl_d(y1, 0);
   const double gZ = shfl_d(y0, 0);
+  PHASE(3)
   const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in));
+  PHASE(4)
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
 #pragma unroll
@@ -509,6 +526,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (c.lane == 31) s = sr;
   double s_left = shfl_up_d(s, 1);
   if (c.lane == 0) s_left = sl;
+  PHASE(5)
   x[CH - 1] = s;
   if (CN) {
     if (regular) chunk_back_raw<CH>(x, P.reg, s_left);
@@ -521,6 +539,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
 #pragma unroll
     for (int j = 0; j < CH; ++j) x[j] = fma(2.0, x[j], -xo[j]);
   }
+  PHASE(6)
 }
 
 // Shared-memory setup common to all kernels. Ends with a cluster barrier so
@@ -985,6 +1004,14 @@ void tri1d_sweep(pint_op *op, const double *prev, double *next, const double *fv
   run_any(TriKind::Sweep, op, 1, op->sweep_cluster, s, nullptr, nullptr, 0, nullptr, gcache, p, prev, next, fv,
           k, deltas, nonfinite, chain);
 }
+
+#ifdef PINT_PHASE_TIMING
+extern "C" int pint_debug_phase_timing(long long *dev_buf, int step) {
+  cudaMemcpyToSymbol(g_phase_buf, &dev_buf, sizeof(dev_buf));
+  cudaMemcpyToSymbol(g_phase_step, &step, sizeof(step));
+  return (int)cudaGetLastError();
+}
+#endif
 
 // Host-only plan export (include/pint_abi.h: pint_tri1d_plan_host).
 extern "C" int pint_tri1d_plan_host(const pint_op_desc *d, int32_t *dims_out, double *fac_out, double *table_out,
