@@ -129,6 +129,8 @@ typedef struct pint_op_info {
   double diag;                 /* 1-D: D of the implicit step matrix */
   double offdiag;              /* 1-D: E of the implicit step matrix */
   double min_pivot;
+  int32_t batch_wave_slices;   /* 1-D: slices apply_batch keeps resident at once (one wave); 0 = unknown */
+  int32_t reserved0;
 } pint_op_info;
 
 int pint_abi_version(void);

@@ -158,6 +158,7 @@ int pint_op_get_info(const pint_op *op, pint_op_info *info) {
     info->diag = op->plan.D;
     info->offdiag = op->plan.E;
     info->min_pivot = op->plan.min_pivot;
+    info->batch_wave_slices = op->batch_wave_slices;
   }
   return PINT_OK;
 }

@@ -87,6 +87,7 @@ struct pint_op {
   double *d_table = nullptr;
   int batch_cluster = 1;
   int sweep_cluster = 1;
+  int batch_wave_slices = 0;  // slices of apply_batch resident at once (0 = unknown)
   int batch_minb = 2;  // CTAs per SM the fine kernel is register-budgeted for (1 or 2)
   // n-D
   int64_t nx = 1, ny = 1, nz = 1;

@@ -868,7 +868,11 @@ static size_t smem_bytes(const Tri1DPlan &pl, int TB) {
   return sizeof(double) * ((size_t)tri1d_nfields(pl.J) * TB + 8 * (size_t)(pl.nW + 1)) + 16;
 }
 
-enum class TriKind { Batch, Init, Sweep };
+enum class TriKind { Batch, Init, Sweep, WaveQuery };
+
+// TriKind::WaveQuery result: clusters of the batch kernel that can be resident
+// at once (cudaOccupancyMaxActiveClusters), i.e. slices per wave
+static thread_local int g_wave_clusters = 0;
 
 template <int CH, int J, bool CN, bool GENERAL>
 static void run_kernel(TriKind kind, const pint_op *op, int grid_slices, int cl, cudaStream_t s,
@@ -889,6 +893,31 @@ static void run_kernel(TriKind kind, const pint_op *op, int grid_slices, int cl,
     case TriKind::Init:
       launch_cluster(tri1d_init_kernel<CH, J, CN, GENERAL>, cl, TB, cl, sm, s, P, lam, gcache, p);
       break;
+    case TriKind::WaveQuery: {
+      auto kern = op->batch_minb == 1 ? tri1d_batch_kernel<CH, J, CN, GENERAL, 1>
+                                      : tri1d_batch_kernel<CH, J, CN, GENERAL, 2>;
+      PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      if (cl > 8) PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg;
+      memset(&cfg, 0, sizeof(cfg));
+      cfg.gridDim = dim3(cl * 1024, 1, 1);
+      cfg.blockDim = dim3(TB, 1, 1);
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      g_wave_clusters = n;
+      break;
+    }
     case TriKind::Sweep:
       launch_cluster(tri1d_sweep_kernel<CH, J, CN, GENERAL>, cl, TB, cl,
                      sm + sizeof(double) * (size_t)TB * (3 * CH + 2), s, P, prev, next, fv, gcache, k, p,
@@ -976,6 +1005,10 @@ void tri1d_setup(pint_op *op) {
     const int v = atoi(bc);
     if (v >= 1 && v <= 16 && pl.T % v == 0 && (pl.T / v) % 32 == 0 && pl.T / v <= 256) op->batch_cluster = v;
   }
+  g_wave_clusters = 0;
+  run_any(TriKind::WaveQuery, op, 1, op->batch_cluster, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr,
+          nullptr, nullptr, 0, nullptr, nullptr);
+  op->batch_wave_slices = g_wave_clusters;
 }
 
 void tri1d_destroy(pint_op *op) {

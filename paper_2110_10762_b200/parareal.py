@@ -20,6 +20,7 @@ G(new) of the same bits (Algorithm 1's w_i^k).
 from __future__ import annotations
 
 import ctypes
+import os
 import json
 from dataclasses import dataclass, field
 
@@ -174,7 +175,7 @@ class SyncEngine:
         self.lam_a = torch.empty(p + 1, n, dtype=fine.dtype, device=dev)
         self.lam_b = torch.empty_like(self.lam_a)
         self.fv = torch.empty_like(self.lam_a)
-        self.gcache = torch.empty_like(self.lam_a)
+        self.gcache = torch.zeros_like(self.lam_a)  # row 0 is never read
         self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
         self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -183,6 +184,19 @@ class SyncEngine:
         self.fused = coarse.is_tridiagonal
         self.prev = self.lam_a
         self.lib = _native.load_library()
+        # pipelining: F runs in wave-sized chunks of slices on the current
+        # stream; each chunk's fused coarse sweep runs on `side` as soon as
+        # its F is done, overlapping the next chunk's F
+        wave = int(getattr(fine.info, "batch_wave_slices", 0)) if fine.is_tridiagonal else 0
+        self.wave = wave if wave > 0 else 0
+        if self.wave and os.environ.get("PINT_SWEEP_CHUNK"):
+            self.wave = max(1, min(self.wave, int(os.environ["PINT_SWEEP_CHUNK"])))
+        self.pipeline = self.fused and self.wave > 0
+        self.side = torch.cuda.Stream(device=dev) if self.pipeline else None
+        self.copy = torch.cuda.Stream(device=dev) if self.pipeline else None
+        # odd F chunks go on a second stream so their clusters start as the
+        # previous chunk's retire (as inside one launch)
+        self.fstream = torch.cuda.Stream(device=dev) if self.pipeline else None
 
     def init(self, u0) -> None:
         self.lam_a[0] = _u0_tensor(self.coarse, u0)
@@ -198,36 +212,132 @@ class SyncEngine:
         if fine_done_event is not None:
             fine_done_event.record(torch.cuda.current_stream(self.fine.device))
 
-    def coarse_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
-        """Fused G chain + correction + per-slice delta for slices [k, p].
-        chain_in: nxt[k-1] and deltas[k-1] already hold this sweep's slice k-1."""
+    def coarse_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False, hi: int | None = None,
+                     stream=None) -> None:
+        """Fused G chain + correction + per-slice delta for slices [k, hi]
+        (hi = p by default). chain_in: nxt[k-1] and deltas[k-1] already hold
+        this sweep's slice k-1 (a previous chunk or another GPU's)."""
         p, prev = self.p, self.prev
+        hi = p if hi is None else int(hi)
         if self.fused:
             fn = self.lib.pint_sync_sweep_chain if chain_in else self.lib.pint_sync_sweep
+            st = _stream(self.coarse) if stream is None else ctypes.c_void_p(stream.cuda_stream)
             rc = fn(self.coarse.handle, ctypes.c_void_p(prev.data_ptr()), ctypes.c_void_p(nxt.data_ptr()),
-                    ctypes.c_void_p(self.fv.data_ptr()), ctypes.c_void_p(self.gcache.data_ptr()), int(k), int(p),
-                    ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()),
-                    _stream(self.coarse))
+                    ctypes.c_void_p(self.fv.data_ptr()), ctypes.c_void_p(self.gcache.data_ptr()), int(k), hi,
+                    ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()), st)
             _native.check(rc, _ctx(self.coarse), "pint_sync_sweep")
         else:
             self._generic_sweep(k, nxt, chain_in)
 
-    def reduce_delta(self, k: int) -> None:
+    def reduce_delta(self, k: int, stream=None) -> None:
+        st = _stream(self.fine) if stream is None else ctypes.c_void_p(stream.cuda_stream)
         rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, self.p + 1,
-                                      ctypes.c_void_p(self.dmax.data_ptr()), _stream(self.fine))
+                                      ctypes.c_void_p(self.dmax.data_ptr()), st)
         _native.check(rc, _ctx(self.fine), "pint_max_reduce")
 
-    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None) -> None:
-        """Sweep k (device work only, stream-ordered): nxt <- new iterate."""
-        self.fine_batch(k, fine_done_event)
-        self.coarse_sweep(k, nxt)
-        self.reduce_delta(k)
+    def chunks(self, k: int) -> list:
+        """Live slices [k, p] split into balanced chunks of at most one wave."""
+        live = self.p - k + 1
+        if not self.pipeline or live <= self.wave:
+            return [(k, self.p)]
+        n = -(-live // self.wave)
+        base, extra = divmod(live, n)
+        out, a = [], k
+        for c in range(n):
+            b = a + base + (1 if c < extra else 0) - 1
+            out.append((a, b))
+            a = b + 1
+        return out
+
+    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None) -> None:
+        """Sweep k (device work only, stream-ordered): nxt <- new iterate.
+        With several chunks, chunk c's coarse sweep overlaps chunk c+1's F.
+        h2d(c, stream) / d2h(c, stream), when given, enqueue chunk c's input
+        upload / result download on the copy stream (sweep_host)."""
+        chunks = self.chunks(k)
+        if len(chunks) == 1 and h2d is None:
+            self.fine_batch(k, fine_done_event)
+            self.coarse_sweep(k, nxt)
+            self.reduce_delta(k)
+            self.prev = nxt
+            return
+        main = torch.cuda.current_stream(self.fine.device)
+        side = self.side if self.side is not None else main
+        cp = self.copy if self.copy is not None else main
+        n = self.fine.dim
+        fs = [main, self.fstream if self.fstream is not None else main]
+        side.wait_stream(main)
+        cp.wait_stream(main)
+        fs[1].wait_stream(main)
+        f_done = []
+        for c, (a, b) in enumerate(chunks):
+            st = fs[c % 2]
+            if h2d is not None:
+                h2d(c, cp)
+                ev = torch.cuda.Event()
+                ev.record(cp)
+                st.wait_event(ev)
+            self.fine.apply_ptr(self.prev[a - 1].data_ptr(), self.fv[a].data_ptr(), b - a + 1, n,
+                                stream=st.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            f_done.append(ev)
+        if fine_done_event is not None:
+            main.wait_stream(fs[1])
+            fine_done_event.record(main)
+        for c, (a, b) in enumerate(chunks):
+            side.wait_event(f_done[c])
+            self.coarse_sweep(a, nxt, chain_in=c > 0, hi=b, stream=side)
+            if c == len(chunks) - 1:
+                self.reduce_delta(k, stream=side)
+            if d2h is not None:
+                ev = torch.cuda.Event()
+                ev.record(side)
+                cp.wait_event(ev)
+                d2h(c, cp)
+        main.wait_stream(fs[1])
+        main.wait_stream(side)
+        main.wait_stream(cp)
         self.prev = nxt
 
-    def launches_per_sweep(self) -> int:
-        """Our kernel launches per sweep (fused path: F batch, coarse sweep,
-        max-reduce)."""
-        return 3 if self.fused else 1 + 3 * self.p
+    def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor) -> float:
+        """One sweep from host (pinned) buffers: host_prev -> device iterate ->
+        sweep -> host_next, with the uploads and downloads of each chunk of
+        slices overlapped with the other chunks' compute. Returns the delta."""
+        chunks = self.chunks(k)
+        rows = []
+        lo = 0
+        for c, (a, b) in enumerate(chunks):
+            hi = self.p if c == len(chunks) - 1 else b
+            rows.append((lo, hi))
+            lo = hi + 1
+        dev_prev = self.lam_a if self.prev is not self.lam_a else self.lam_b
+        nxt = self.lam_b if dev_prev is self.lam_a else self.lam_a
+
+        def h2d(c, st):
+            r0, r1 = rows[c]
+            with torch.cuda.stream(st):
+                dev_prev[r0:r1 + 1].copy_(host_prev[r0:r1 + 1], non_blocking=True)
+
+        def d2h(c, st):
+            r0, r1 = rows[c]
+            with torch.cuda.stream(st):
+                host_next[r0:r1 + 1].copy_(nxt[r0:r1 + 1], non_blocking=True)
+                if c == len(rows) - 1:
+                    self.host[:1].copy_(self.dmax, non_blocking=True)
+                    self.host[1:2].copy_(self.flag.to(torch.float64), non_blocking=True)
+
+        self.prev = dev_prev
+        self.sweep(k, nxt, h2d=h2d, d2h=d2h)
+        torch.cuda.current_stream(self.fine.device).synchronize()
+        if self.host[1].item() != 0.0:
+            raise ValueError("block entries must be finite")
+        return float(self.host[0].item())
+
+    def launches_per_sweep(self, k: int = 1) -> int:
+        """Our kernel launches per sweep (fused path: F batch and coarse sweep
+        per chunk, max-reduce)."""
+        return 2 * len(self.chunks(k)) + 1 if self.fused else 1 + 3 * self.p
 
     def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
         """Coarse chain + correction for coarse operators without a fused

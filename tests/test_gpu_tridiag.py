@@ -103,3 +103,66 @@ def test_fixture_exact_termination_bitwise(gpu, n):
         for k in range(1, len(tr.iterates)):
             for i in range(0, k + 1):
                 assert np.array_equal(tr.iterates[k].data[i], seq.data[i])
+
+
+@pytest.mark.parametrize("wave", [1, 3, 5])
+def test_pipelined_sweep_is_bitwise_the_single_launch_sweep(gpu, wave):
+    """Chunked F + overlapped chunked coarse sweeps (chain input across chunk
+    boundaries) give the same bits as one F launch + one fused sweep, for
+    several sweeps (frozen prefixes k = 1..4)."""
+    import torch
+    from oracle import heat_oracle as H
+    from paper_2110_10762_b200.parareal import SyncEngine
+    n, p = 1024, 16
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 100)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    assert fine.info.batch_wave_slices > 0
+    ref = SyncEngine(coarse, fine, p)
+    ref.pipeline = False
+    eng = SyncEngine(coarse, fine, p)
+    eng.wave, eng.pipeline = wave, True
+    eng.side, eng.copy = torch.cuda.Stream(), torch.cuda.Stream()
+    for e in (ref, eng):
+        e.init(u0)
+    for k in range(1, 5):
+        outs = []
+        for e in (ref, eng):
+            nxt = e.lam_b if e.prev is e.lam_a else e.lam_a
+            nxt.copy_(e.prev)
+            e.sweep(k, nxt)
+            outs.append((nxt.clone(), e.read_delta(), e.deltas.clone(), e.gcache.clone()))
+        assert len(eng.chunks(k)) == -(-(p - k + 1) // wave)
+        assert torch.equal(outs[0][0], outs[1][0]), k
+        assert outs[0][1] == outs[1][1]
+        assert torch.equal(outs[0][2], outs[1][2])
+        assert torch.equal(outs[0][3][1:], outs[1][3][1:])  # G(old) of slices 1..p (row 0 is never used)
+
+
+def test_sweep_host_matches_device_sweep(gpu):
+    """The host-buffer sweep (pinned uploads/downloads overlapped per chunk)
+    returns the device sweep's iterate and delta bitwise."""
+    import torch
+    from oracle import heat_oracle as H
+    from paper_2110_10762_b200.parareal import SyncEngine
+    n, p = 4096, 12
+    u0 = H.sine_u0_1d(n, 8, 1)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 50)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    ref = SyncEngine(coarse, fine, p)
+    ref.init(u0)
+    host_in = ref.lam_a.cpu().pin_memory()
+    g0 = ref.gcache.clone()
+    ref.sweep(1, ref.lam_b)
+    want, dwant = ref.lam_b.cpu(), ref.read_delta()
+    eng = SyncEngine(coarse, fine, p)
+    eng.init(u0)
+    eng.gcache.copy_(g0)
+    eng.wave, eng.pipeline = 5, True
+    eng.side, eng.copy = torch.cuda.Stream(), torch.cuda.Stream()
+    host_out = torch.empty_like(host_in).pin_memory()
+    d = eng.sweep_host(1, host_in, host_out)
+    assert d == dwant
+    assert torch.equal(host_out, want)
