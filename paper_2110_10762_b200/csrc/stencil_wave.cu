@@ -56,11 +56,24 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   const T four = T(4);
   const int ys = y0 - S, ye = min(y0 + YC2, ny) - 1 + S;
   int par = 0;
+  // input rows are prefetched one iteration ahead (the load latency would
+  // otherwise sit in front of every row's barrier)
+  T pre[CPT2];
+  {
+    const bool rowin = ys >= 0 && ys < ny;
+#pragma unroll
+    for (int c = 0; c < CPT2; ++c) pre[c] = (rowin && colin[c]) ? __ldg(src + (int64_t)ys * nx + cx + c) : T(0);
+  }
   for (int yy = ys; yy <= ye; ++yy, par ^= 1) {
     // level 0: the input row yy
-    const bool rowin = yy >= 0 && yy < ny;
 #pragma unroll
-    for (int c = 0; c < CPT2; ++c) cur[0][c] = (rowin && colin[c]) ? __ldg(src + (int64_t)yy * nx + cx + c) : T(0);
+    for (int c = 0; c < CPT2; ++c) cur[0][c] = pre[c];
+    {
+      const int yn = yy + 1;
+      const bool rowin = yn >= 0 && yn < ny && yn <= ye;
+#pragma unroll
+      for (int c = 0; c < CPT2; ++c) pre[c] = (rowin && colin[c]) ? __ldg(src + (int64_t)yn * nx + cx + c) : T(0);
+    }
 #pragma unroll
     for (int c = 0; c < CPT2; ++c) sm[par][0][1 + CPT2 * tid + c] = cur[0][c];
     // levels 1..S: level L+1 at row yy-L-1 from level L rows (pp, prv, cur)
@@ -152,108 +165,201 @@ template void fe2d_wave_apply<double>(const pint_op *, const double *, double *,
                                       cudaStream_t);
 
 // --------------------------------------------------------------- 3-D (7-point)
-// Same wavefront with z as the sweep axis: a CTA owns an xy tile (plus S
-// halo cells per side) of z-columns and a chunk of z planes; each thread owns
-// CPT3 x-adjacent columns and carries S levels x 3 planes in registers; the
-// xy neighbours of a level's previous plane come from a double-buffered
-// shared tile. HBM traffic 2*sizeof(T)/S bytes per update; the halo costs
-// (BX3+2S)(BY3+2S)/(BX3 BY3) redundant updates.
+// Same wavefront with z as the sweep axis. A CTA owns an xy tile of z-columns
+// (64 columns x RW rows, including S halo cells per side) and a chunk of ZC3
+// z planes; warp w owns tile row w and each lane two adjacent columns, so
+// x-neighbours come from warp shuffles (lane +-1), y-neighbours from the rows
+// above/below in a double-buffered shared tile (8-byte vector accesses, no
+// bank conflicts) and z-neighbours from registers (three planes per level).
+// One barrier per plane. HBM traffic 2*sizeof(T)/S bytes per update; the
+// halo costs 64 RW / ((64 - 2S)(RW - 2S)) redundant xy updates and
+// (ZC3 + 2S) / ZC3 in z. Values outside the domain are the Dirichlet zeros;
+// out-of-tile neighbours read 0 (only halo cells see them).
 namespace {
 
 constexpr int SMAX3 = 4;
 constexpr int CPT3 = 2;
-constexpr int BX3 = 64, BY3 = 16;
-constexpr int WX3 = BX3 + 2 * SMAX3, WY3 = BY3 + 2 * SMAX3;  // 72 x 24 loaded columns
-constexpr int TX3 = WX3 / CPT3;                               // 36 threads in x
-constexpr int ZC3 = 64;                                        // output planes per chunk
+constexpr int W3 = 32 * CPT3;  // tile columns (incl. halo)
+constexpr int ZC3 = 128;       // output planes per chunk
 
-template <typename T, int S>
-__global__ void __launch_bounds__(TX3 *WY3)
-fe3d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, int nz, T r, int tiles_x) {
-  extern __shared__ __align__(16) unsigned char smraw3[];
-  T(*sm)[S][WY3 + 2][WX3 + 2] = reinterpret_cast<T(*)[S][WY3 + 2][WX3 + 2]>(smraw3);
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tid = ty * TX3 + tx;
-  const int bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
-  const int x0 = bx * BX3 - S, y0 = by * BY3 - S, z0 = blockIdx.y * ZC3;
-  const int64_t plane = (int64_t)nx * ny;
-  const T *src = in + (int64_t)blockIdx.z * stride;
-  T *dst = out + (int64_t)blockIdx.z * stride;
-  const int cx = x0 + CPT3 * tx, cy = y0 + ty;
-  bool colin[CPT3], colout[CPT3];
-#pragma unroll
-  for (int c = 0; c < CPT3; ++c) {
-    colin[c] = cx + c >= 0 && cx + c < nx && cy >= 0 && cy < ny;
-    const int lx = CPT3 * tx + c;
-    colout[c] = colin[c] && lx >= S && lx < S + BX3 && ty >= S && ty < S + BY3;
-  }
-  for (int i = tid; i < 2 * S * (WY3 + 2) * (WX3 + 2); i += TX3 * WY3) (&sm[0][0][0][0])[i] = T(0);
-  T cur[S][CPT3], prv[S][CPT3], pp[S][CPT3];
-#pragma unroll
-  for (int L = 0; L < S; ++L)
-#pragma unroll
-    for (int c = 0; c < CPT3; ++c) cur[L][c] = prv[L][c] = pp[L][c] = T(0);
-  __syncthreads();
+// packed FP32 pairs (FADD2 / FFMA2 / FMUL2 on sm_100a): the two columns of
+// a lane in one instruction, same per-element IEEE result as scalar code
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> { using V = float2; };
+template <>
+struct Pair<double> { using V = double2; };
+
+// One plane of the wavefront (input plane zz arrives; level L+1 is advanced
+// at plane zz-L-1). EDGE: some level's plane lies outside the domain (the
+// first/last S planes of the sweep), so the plane mask is applied per level;
+// PAR: shared buffer parity (compile time, the caller unrolls by two).
+template <typename T, int S, int RW, bool EDGE, int PAR>
+__device__ __forceinline__ void plane3(T (&cur)[S][CPT3], T (&prv)[S][CPT3], T (&pp)[S][CPT3], T (&pre)[CPT3],
+                                       typename Pair<T>::V (*sm)[S][RW][32], int w, int w_up, int w_dn, int lane,
+                                       const bool (&colin)[CPT3], const bool (&colout)[CPT3], int zz, int z0,
+                                       int nz, int ze, const T *src, T *dst, int64_t plane, int64_t col, T r) {
+  using V = typename Pair<T>::V;
   const T six = T(6);
-  const int zs = z0 - S, ze = min(z0 + ZC3, nz) - 1 + S;
-  const int sx = 1 + CPT3 * tx, sy = 1 + ty;
-  int par = 0;
-  for (int zz = zs; zz <= ze; ++zz, par ^= 1) {
-    const bool pin = zz >= 0 && zz < nz;
 #pragma unroll
-    for (int c = 0; c < CPT3; ++c) {
-      cur[0][c] = (pin && colin[c]) ? __ldg(src + (int64_t)zz * plane + (int64_t)cy * nx + cx + c) : T(0);
-      sm[par][0][sy][sx + c] = cur[0][c];
-    }
+  for (int c = 0; c < CPT3; ++c) cur[0][c] = pre[c];
+  sm[PAR][0][w][lane] = V{cur[0][0], cur[0][1]};
+  {
+    const int zn = zz + 1;
+    const bool pin = zn >= 0 && zn < nz && zn <= ze;
 #pragma unroll
-    for (int L = 0; L < S; ++L) {
-      const int zr = zz - L - 1;
-      const bool rin = zr >= 0 && zr < nz;
-      const T left = sm[par ^ 1][L][sy][sx - 1];
-      const T right = sm[par ^ 1][L][sy][sx + CPT3];
-      T v[CPT3];
+    for (int c = 0; c < CPT3; ++c) pre[c] = (pin && colin[c]) ? __ldg(src + (int64_t)zn * plane + col + c) : T(0);
+  }
+#pragma unroll
+  for (int L = 0; L < S; ++L) {
+    const int zr = zz - L - 1;
+    const bool rin = !EDGE || (zr >= 0 && zr < nz);
+    // out-of-tile neighbours (lane 0/31 shuffles, clamped rows) are garbage
+    // that only reaches halo cells
+    const T left = __shfl_up_sync(0xffffffffu, prv[L][CPT3 - 1], 1);
+    const T right = __shfl_down_sync(0xffffffffu, prv[L][0], 1);
+    const V up = sm[PAR ^ 1][L][w_up][lane];
+    const V dn = sm[PAR ^ 1][L][w_dn][lane];
+    T v[CPT3];
+    if constexpr (sizeof(T) == 4) {
+      // ((xl + xr) + (up + dn)) + (pz + nz), then ctr + r (nb - 6 ctr): the scalar path's order
+      const unsigned long long ctr = pk2(prv[L][0], prv[L][1]);
+      const unsigned long long nb = add2(add2(add2(pk2(left, prv[L][0]), pk2(prv[L][1], right)),
+                                              add2(pk2(up.x, up.y), pk2(dn.x, dn.y))),
+                                         add2(pk2(pp[L][0], pp[L][1]), pk2(cur[L][0], cur[L][1])));
+      const unsigned long long t = fma2(pk2(-six, -six), ctr, nb);
+      unsigned long long vv = fma2(pk2(r, r), t, ctr);
+      const float m0 = (rin && colin[0]) ? 1.0f : 0.0f, m1 = (rin && colin[1]) ? 1.0f : 0.0f;
+      vv = mul2(vv, pk2(m0, m1));
+      const float2 f = upk2(vv);
+      v[0] = f.x;
+      v[1] = f.y;
+    } else {
+      const T upv[2] = {up.x, up.y}, dnv[2] = {dn.x, dn.y};
 #pragma unroll
       for (int c = 0; c < CPT3; ++c) {
         const T ctr = prv[L][c];
         const T xl = (c == 0) ? left : prv[L][c - 1];
         const T xr = (c == CPT3 - 1) ? right : prv[L][c + 1];
-        const T yl = sm[par ^ 1][L][sy - 1][sx + c];
-        const T yr = sm[par ^ 1][L][sy + 1][sx + c];
-        const T nb = ((xl + xr) + (yl + yr)) + (pp[L][c] + cur[L][c]);
+        const T nb = ((xl + xr) + (upv[c] + dnv[c])) + (pp[L][c] + cur[L][c]);
         v[c] = (rin && colin[c]) ? ctr + r * (nb - six * ctr) : T(0);
       }
-      if (L + 1 < S) {
-#pragma unroll
-        for (int c = 0; c < CPT3; ++c) {
-          cur[L + 1][c] = v[c];
-          sm[par][L + 1][sy][sx + c] = v[c];
-        }
-      } else if (zr >= z0 && zr < z0 + ZC3 && rin) {
-#pragma unroll
-        for (int c = 0; c < CPT3; ++c)
-          if (colout[c]) dst[(int64_t)zr * plane + (int64_t)cy * nx + cx + c] = v[c];
-      }
     }
+    if (L + 1 < S) {
 #pragma unroll
-    for (int L = 0; L < S; ++L)
+      for (int c = 0; c < CPT3; ++c) cur[L + 1][c] = v[c];
+      sm[PAR][L + 1][w][lane] = V{v[0], v[1]};
+    } else if (zr >= z0 && zr < z0 + ZC3 && rin) {
 #pragma unroll
-      for (int c = 0; c < CPT3; ++c) {
-        pp[L][c] = prv[L][c];
-        prv[L][c] = cur[L][c];
-      }
-    __syncthreads();
+      for (int c = 0; c < CPT3; ++c)
+        if (colout[c]) dst[(int64_t)zr * plane + col + c] = v[c];
+    }
+  }
+#pragma unroll
+  for (int L = 0; L < S; ++L)
+#pragma unroll
+    for (int c = 0; c < CPT3; ++c) {
+      pp[L][c] = prv[L][c];
+      prv[L][c] = cur[L][c];
+    }
+  __syncthreads();
+}
+
+template <typename T, int S, int RW>
+__global__ void __launch_bounds__(32 * RW)
+fe3d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, int nz, T r, int tiles_x) {
+  using V = typename Pair<T>::V;
+  extern __shared__ __align__(16) unsigned char smraw3[];
+  V(*sm)[S][RW][32] = reinterpret_cast<V(*)[S][RW][32]>(smraw3);  // [par][level][row][lane] pairs
+  constexpr int BX = W3 - 2 * S, BY = RW - 2 * S;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int w_up = w > 0 ? w - 1 : 0, w_dn = w < RW - 1 ? w + 1 : RW - 1;
+  const int bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
+  const int x0 = bx * BX - S, y0 = by * BY - S, z0 = blockIdx.y * ZC3;
+  const int64_t plane = (int64_t)nx * ny;
+  const T *src = in + (int64_t)blockIdx.z * stride;
+  T *dst = out + (int64_t)blockIdx.z * stride;
+  const int cx = x0 + CPT3 * lane, cy = y0 + w;
+  bool colin[CPT3], colout[CPT3];
+#pragma unroll
+  for (int c = 0; c < CPT3; ++c) {
+    colin[c] = cx + c >= 0 && cx + c < nx && cy >= 0 && cy < ny;
+    const int lx = CPT3 * lane + c;
+    colout[c] = colin[c] && lx >= S && lx < S + BX && w >= S && w < S + BY;
+  }
+  T cur[S][CPT3], prv[S][CPT3], pp[S][CPT3];
+#pragma unroll
+  for (int L = 0; L < S; ++L)
+#pragma unroll
+    for (int c = 0; c < CPT3; ++c) cur[L][c] = prv[L][c] = pp[L][c] = T(0);
+  // both parities of every level start at 0 (the first planes read them)
+  for (int i = threadIdx.x; i < 2 * S * RW * 32; i += 32 * RW) (&sm[0][0][0][0])[i] = V{T(0), T(0)};
+  __syncthreads();
+  const int zs = z0 - S, ze = min(z0 + ZC3, nz) - 1 + S;
+  const int64_t col = (int64_t)cy * nx + cx;
+  T pre[CPT3];  // next input plane, prefetched one iteration ahead
+  {
+    const bool pin = zs >= 0 && zs < nz;
+#pragma unroll
+    for (int c = 0; c < CPT3; ++c) pre[c] = (pin && colin[c]) ? __ldg(src + (int64_t)zs * plane + col + c) : T(0);
+  }
+  // planes zz in [S, nz] have every level's plane inside the domain
+  for (int zz = zs; zz <= ze; zz += 2) {
+    if (zz >= S && zz + 1 <= nz)
+      plane3<T, S, RW, false, 0>(cur, prv, pp, pre, sm, w, w_up, w_dn, lane, colin, colout, zz, z0, nz, ze, src, dst,
+                                 plane, col, r);
+    else
+      plane3<T, S, RW, true, 0>(cur, prv, pp, pre, sm, w, w_up, w_dn, lane, colin, colout, zz, z0, nz, ze, src, dst,
+                                plane, col, r);
+    if (zz + 1 > ze) break;
+    if (zz + 1 >= S && zz + 1 <= nz)
+      plane3<T, S, RW, false, 1>(cur, prv, pp, pre, sm, w, w_up, w_dn, lane, colin, colout, zz + 1, z0, nz, ze, src,
+                                 dst, plane, col, r);
+    else
+      plane3<T, S, RW, true, 1>(cur, prv, pp, pre, sm, w, w_up, w_dn, lane, colin, colout, zz + 1, z0, nz, ze, src,
+                                dst, plane, col, r);
   }
 }
 
 template <typename T, int S>
 void launch3(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, int nz, T r, cudaStream_t st) {
-  const int tiles_x = (nx + BX3 - 1) / BX3, tiles_y = (ny + BY3 - 1) / BY3;
+  // fp32: 32 rows (1024 threads); fp64: 16 rows (register budget)
+  constexpr int RW = sizeof(T) == 4 ? 32 : 16;
+  constexpr int BX = W3 - 2 * S, BY = RW - 2 * S;
+  const int tiles_x = (nx + BX - 1) / BX, tiles_y = (ny + BY - 1) / BY;
   const unsigned tz = (unsigned)((nz + ZC3 - 1) / ZC3);
-  const size_t smem = sizeof(T) * 2 * S * (WY3 + 2) * (WX3 + 2);
-  PINT_CUDA(cudaFuncSetAttribute(fe3d_wave<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = sizeof(T) * 2 * 2 * S * RW * 32;
+  PINT_CUDA(cudaFuncSetAttribute(fe3d_wave<T, S, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
     const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
-    fe3d_wave<T, S><<<dim3((unsigned)(tiles_x * tiles_y), tz, n), dim3(TX3, WY3), smem, st>>>(
+    fe3d_wave<T, S, RW><<<dim3((unsigned)(tiles_x * tiles_y), tz, n), 32 * RW, smem, st>>>(
         in + b0 * stride, out + b0 * stride, stride, nx, ny, nz, r, tiles_x);
   }
   PINT_CUDA(cudaGetLastError());
