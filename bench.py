@@ -375,6 +375,9 @@ def time_to_tolerance(coarse, fine, u0, p: int, eps: float = 1e-10) -> dict:
         out["async_device"] = {"error": f"{type(exc).__name__}: {exc}"}
     costs = pb.measure_costs(coarse, fine, p)
     out["cost_model"] = pb.model_report(costs, p, k=tr.k_final, kappa=kappa, measured_sync_s=wall)
+    rep = pb.contraction_factors(coarse, fine, p)  # matrix-free spectral norms at full size
+    out["contraction"] = rep.to_dict() | {"sync_check": list(pb.sync_convergence_check(rep)),
+                                           "async_check": list(pb.async_convergence_check(rep))}
     return out
 
 

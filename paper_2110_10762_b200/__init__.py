@@ -40,8 +40,20 @@ from .errors import (
     NativeLibraryError,
     SingularMatrixError,
     SingularSystemError,
+    InvalidThetaError,
     UndefinedLimitError,
     UnfittableError,
+)
+from .contraction import (
+    CheckResult,
+    ContractionReport,
+    NormKind,
+    RateComparison,
+    async_convergence_check,
+    compare_factors,
+    contraction_factors,
+    factors_from_norms,
+    sync_convergence_check,
 )
 from .costmodel import (
     CostParams,

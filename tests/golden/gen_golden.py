@@ -185,7 +185,41 @@ def async_traces():
     save("async_traces.npz", **out)
 
 
+def contraction():
+    """pintlab.analysis.contraction_factors (analysis.py:92-98, spectral norm
+    by Gram power iteration) on the C1 propagators, a trapezoidal/BE pair
+    and a reduced 2-D explicit/implicit pair."""
+    from pintlab.analysis import contraction_factors
+    from pintlab.linalg import NormKind
+    out = {}
+    cases = []
+    n, p, T = 1024, 16, 1.0
+    ivp = LinearIVP(heat1d_system(n, 1.0, 0.0, 0.0, 0.0, T).a_mat, np.zeros(n), np.zeros(n), T)
+    cases.append(("c1", ivp, backward_euler_propagator(ivp, T / p, 100), backward_euler_propagator(ivp, T / p, 1),
+                  p, dict(shape=[n], fine=["backward-euler", T / p / 100, 100], coarse=["backward-euler", T / p, 1])))
+    n, p = 64, 8
+    ivp = LinearIVP(heat1d_system(n, 1.0, 0.0, 0.0, 0.0, T).a_mat, np.zeros(n), np.zeros(n), T)
+    cases.append(("cn64", ivp, trapezoidal_propagator(ivp, T / p, 50), backward_euler_propagator(ivp, T / p, 1),
+                  p, dict(shape=[n], fine=["trapezoidal", T / p / 50, 50], coarse=["backward-euler", T / p, 1])))
+    n, p, steps = 12, 8, 40
+    h = 1.0 / (n + 1)
+    dt = 0.2 * h * h
+    a = kron_laplacian((n, n), h)
+    ivp2 = LinearIVP(a, np.zeros(n * n), np.zeros(n * n), p * steps * dt)
+    one = AffinePropagator(np.eye(n * n) + dt * a, np.zeros(n * n), 1.0)
+    cases.append(("fe2d", ivp2, fine_from_onestep(one, steps), backward_euler_propagator(ivp2, steps * dt, 1),
+                  p, dict(shape=[n, n], fine=["forward-euler", dt, steps],
+                          coarse=["backward-euler", steps * dt, 1])))
+    for tag, _, fine, coarse, pp, meta in cases:
+        for kind in (NormKind.SPECTRAL, NormKind.INFINITY):
+            r = contraction_factors(coarse, fine, pp, kind=kind)
+            out[f"{tag}_{kind.value}"] = np.array([r.coarse_norm, r.defect_norm, r.sync_factor, r.async_factor])
+        out[f"{tag}_meta"] = np.array(json.dumps(meta | {"p": pp, "length": 1.0}))
+    save("contraction.npz", **out)
+
+
 if __name__ == "__main__":
+    contraction()
     c1()
     fixtures()
     one_d_layouts()
