@@ -336,7 +336,7 @@ def run_ours(args, rank: int, world: int) -> None:
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
-        if args.time_to_tol:
+        if args.time_to_tol and world == 1:
             line["time_to_tolerance"] = time_to_tolerance(coarse, fine, u0, P_LOCAL)
         print(json.dumps(line), flush=True)
 
@@ -388,7 +388,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--time-to-tol", action="store_true")
+    ap.add_argument("--time-to-tol", action="store_true", default=True,
+                    help="sync + device-async time to tolerance, cost model, contraction factors (default on)")
+    ap.add_argument("--no-time-to-tol", dest="time_to_tol", action="store_false")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
