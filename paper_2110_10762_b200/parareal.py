@@ -194,6 +194,7 @@ class SyncEngine:
         self.pipeline = self.fused and self.wave > 0
         self.side = torch.cuda.Stream(device=dev) if self.pipeline else None
         self.copy = torch.cuda.Stream(device=dev) if self.pipeline else None
+        self.dcopy = torch.cuda.Stream(device=dev) if self.pipeline else None  # downloads (other PCIe direction)
         # odd F chunks go on a second stream so their clusters start as the
         # previous chunk's retire (as inside one launch)
         self.fstream = torch.cuda.Stream(device=dev) if self.pipeline else None
@@ -249,13 +250,16 @@ class SyncEngine:
             a = b + 1
         return out
 
-    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None) -> None:
+    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None,
+              d2h_splits: int = 1) -> None:
         """Sweep k (device work only, stream-ordered): nxt <- new iterate.
         With several chunks, chunk c's coarse sweep overlaps chunk c+1's F.
-        h2d(c, stream) / d2h(c, stream), when given, enqueue chunk c's input
-        upload / result download on the copy stream (sweep_host)."""
+        h2d(c, stream) enqueues chunk c's input upload before its F;
+        d2h(lo, hi, last, stream) enqueues the download of slices [lo, hi]
+        as soon as the coarse sweep has produced them (the last chunk's sweep
+        is split into d2h_splits launches so its download overlaps it)."""
         chunks = self.chunks(k)
-        if len(chunks) == 1 and h2d is None:
+        if len(chunks) == 1 and h2d is None and d2h is None:
             self.fine_batch(k, fine_done_event)
             self.coarse_sweep(k, nxt)
             self.reduce_delta(k)
@@ -264,10 +268,12 @@ class SyncEngine:
         main = torch.cuda.current_stream(self.fine.device)
         side = self.side if self.side is not None else main
         cp = self.copy if self.copy is not None else main
+        dn = self.dcopy if getattr(self, "dcopy", None) is not None else cp
         n = self.fine.dim
         fs = [main, self.fstream if self.fstream is not None else main]
         side.wait_stream(main)
         cp.wait_stream(main)
+        dn.wait_stream(main)
         fs[1].wait_stream(main)
         f_done = []
         for c, (a, b) in enumerate(chunks):
@@ -285,25 +291,36 @@ class SyncEngine:
         if fine_done_event is not None:
             main.wait_stream(fs[1])
             fine_done_event.record(main)
+        lo = 0
         for c, (a, b) in enumerate(chunks):
             side.wait_event(f_done[c])
-            self.coarse_sweep(a, nxt, chain_in=c > 0, hi=b, stream=side)
-            if c == len(chunks) - 1:
-                self.reduce_delta(k, stream=side)
-            if d2h is not None:
-                ev = torch.cuda.Event()
-                ev.record(side)
-                cp.wait_event(ev)
-                d2h(c, cp)
+            last = c == len(chunks) - 1
+            parts = max(1, min(int(d2h_splits), b - a + 1)) if (last and d2h is not None) else 1
+            base, extra = divmod(b - a + 1, parts)
+            pa = a
+            for q in range(parts):
+                pb = pa + base + (1 if q < extra else 0) - 1
+                self.coarse_sweep(pa, nxt, chain_in=(c > 0 or q > 0), hi=pb, stream=side)
+                if last and q == parts - 1:
+                    self.reduce_delta(k, stream=side)
+                if d2h is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    dn.wait_event(ev)
+                    d2h(lo, pb, last and q == parts - 1, dn)
+                    lo = pb + 1
+                pa = pb + 1
         main.wait_stream(fs[1])
         main.wait_stream(side)
         main.wait_stream(cp)
+        main.wait_stream(dn)
         self.prev = nxt
 
-    def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor) -> float:
+    def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor, d2h_splits: int = 4) -> float:
         """One sweep from host (pinned) buffers: host_prev -> device iterate ->
-        sweep -> host_next, with the uploads and downloads of each chunk of
-        slices overlapped with the other chunks' compute. Returns the delta."""
+        sweep -> host_next. Each chunk's upload overlaps the previous chunk's
+        F; downloads follow the coarse sweep in pieces on their own stream.
+        Returns the delta."""
         chunks = self.chunks(k)
         rows = []
         lo = 0
@@ -319,16 +336,15 @@ class SyncEngine:
             with torch.cuda.stream(st):
                 dev_prev[r0:r1 + 1].copy_(host_prev[r0:r1 + 1], non_blocking=True)
 
-        def d2h(c, st):
-            r0, r1 = rows[c]
+        def d2h(r0, r1, final, st):
             with torch.cuda.stream(st):
                 host_next[r0:r1 + 1].copy_(nxt[r0:r1 + 1], non_blocking=True)
-                if c == len(rows) - 1:
+                if final:
                     self.host[:1].copy_(self.dmax, non_blocking=True)
                     self.host[1:2].copy_(self.flag.to(torch.float64), non_blocking=True)
 
         self.prev = dev_prev
-        self.sweep(k, nxt, h2d=h2d, d2h=d2h)
+        self.sweep(k, nxt, h2d=h2d, d2h=d2h, d2h_splits=d2h_splits)
         torch.cuda.current_stream(self.fine.device).synchronize()
         if self.host[1].item() != 0.0:
             raise ValueError("block entries must be finite")
@@ -338,6 +354,14 @@ class SyncEngine:
         """Our kernel launches per sweep (fused path: F batch and coarse sweep
         per chunk, max-reduce)."""
         return 2 * len(self.chunks(k)) + 1 if self.fused else 1 + 3 * self.p
+
+    def launches_per_host_sweep(self, k: int = 1, d2h_splits: int = 4) -> int:
+        """As launches_per_sweep, for sweep_host (the last chunk's coarse
+        sweep is split into d2h_splits launches)."""
+        ch = self.chunks(k)
+        a, b = ch[-1]
+        # F per chunk + coarse sweep per chunk (the last one split) + max-reduce
+        return 2 * len(ch) + min(d2h_splits, b - a + 1) if self.fused else 1 + 3 * self.p
 
     def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
         """Coarse chain + correction for coarse operators without a fused
