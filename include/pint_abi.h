@@ -26,6 +26,11 @@
  *                               simulate_async event loop, async_engine.py:238-365)
  *   pint_async_run_traced   <- + AsyncTrace / UpdateRecord  async_engine.py:122-190
  *                              (audited as validate_schedule, async_engine.py:402-459)
+ *   pint_async_domain_*     <- run_async_parareal across GPUs (one domain of
+ *                              contiguous slices per GPU; the slice-boundary
+ *                              state is pushed to the next GPU by P2P stores;
+ *                              no reference counterpart: the reference is
+ *                              single-process, async_engine.py:238-365)
  *
  * Error codes map onto the reference's exception taxonomy (errors.py):
  *   PINT_EDIM       -> DimensionError                errors.py:10-11
@@ -80,6 +85,7 @@ enum pint_rule {
 
 typedef struct pint_ctx pint_ctx;
 typedef struct pint_op pint_op;
+typedef struct pint_async_domain pint_async_domain;
 
 /*
  * Operator description. The operator is u' = A u + c on a tensor grid of
@@ -240,6 +246,59 @@ int pint_async_run_traced(pint_op *fine, pint_op *coarse, const void *lam0,
                           double delay_frac, uint64_t seed, void *final_out,
                           int64_t *counts_out, int64_t *info_out,
                           int64_t *trace_out, int64_t trace_cap, void *stream);
+
+/*
+ * Multi-GPU asynchronous runtime. One DOMAIN = the contiguous
+ * slices lo..hi (1-based) owned by one GPU, plus a ghost row (mailbox) for
+ * slice lo-1. The domain's workspace is one cudaMalloc block whose layout
+ * depends only on (hi-lo+1, N, world, clusters, trace_cap), so peers address
+ * each other's mailbox and status board from the exported base pointer.
+ * Sequence per rank (distributed.py): create -> ipc_handle -> exchange
+ * handles (host) -> connect -> reset -> host barrier -> launch -> stream
+ * sync -> host barrier -> collect -> destroy. Domains hosted by one process
+ * on one device are wired with pint_async_domains_connect_local and launched
+ * together (the single-GPU emulation of a multi-GPU run).
+ */
+int pint_async_domain_create(pint_op *fine, pint_op *coarse, int64_t p,
+                             int64_t lo, int64_t hi, int world, int index,
+                             int64_t nclusters, int64_t trace_cap,
+                             pint_async_domain **out);
+/* handle_out: 64 bytes (cudaIpcMemHandle_t of the workspace). */
+int pint_async_domain_ipc_handle(pint_async_domain *dom, void *handle_out);
+/* handles: world x 64 bytes (own entry ignored); nloc_all: world slice counts. */
+int pint_async_domain_connect(pint_async_domain *dom, const void *handles,
+                              const int64_t *nloc_all);
+/* doms[x] must have index x, x = 0..ndom-1 == world. */
+int pint_async_domains_connect_local(int ndom, pint_async_domain **doms);
+/* rows: device, (hi-lo+2) x N = coarse initial iterate lam0[lo-1 .. hi]. Synchronous. */
+int pint_async_domain_reset(pint_async_domain *dom, const void *rows, void *stream);
+/* One persistent launch hosting ndom connected domains of the calling device. */
+int pint_async_domain_launch(int ndom, pint_async_domain **doms, double epsilon,
+                             int64_t max_events, double delay_frac,
+                             uint64_t seed, void *stream);
+/*
+ * After the launch completed: rows_out (device, (hi-lo+2) x N) <- newest
+ * published rows lo-1..hi (row 0 = ghost); counts_out (host, hi-lo+2);
+ * info_out (host, 6) = {global activations, stop code, non-finite, seqlock
+ * retries, clusters, local activations}; trace_out (host) <- records at
+ * global event positions (zeros where another GPU published).
+ */
+int pint_async_domain_collect(pint_async_domain *dom, void *rows_out,
+                              int64_t *counts_out, int64_t *info_out,
+                              int64_t *trace_out, int64_t trace_cap,
+                              void *stream);
+int pint_async_domain_destroy(pint_async_domain *dom);
+/*
+ * pint_async_run_traced over ndom domains hosted by ONE launch on the calling
+ * device (ndom = 1 is pint_async_run_traced): the multi-GPU protocol
+ * (mailbox push, status boards, distributed stop) emulated on one GPU.
+ */
+int pint_async_run_domains(pint_op *fine, pint_op *coarse, const void *lam0,
+                           int64_t p, int ndom, double epsilon,
+                           int64_t max_events, double delay_frac,
+                           uint64_t seed, void *final_out, int64_t *counts_out,
+                           int64_t *info_out, int64_t *trace_out,
+                           int64_t trace_cap, void *stream);
 
 /* max over deltas_dev[lo..hi) -> *out_dev (device double), deterministic. */
 int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,

@@ -81,6 +81,17 @@ SIGNATURES = {
                                c_void_p, c_void_p, c_void_p, c_void_p]),
     "pint_async_run_traced": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_double, c_i64, c_double,
                                       ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p]),
+    "pint_async_domain_create": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_i64, c_int, c_int, c_i64, c_i64,
+                                         ctypes.POINTER(c_void_p)]),
+    "pint_async_domain_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "pint_async_domain_connect": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "pint_async_domains_connect_local": (c_int, [c_int, c_void_p]),
+    "pint_async_domain_reset": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "pint_async_domain_launch": (c_int, [c_int, c_void_p, c_double, c_i64, c_double, ctypes.c_uint64, c_void_p]),
+    "pint_async_domain_collect": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p]),
+    "pint_async_domain_destroy": (c_int, [c_void_p]),
+    "pint_async_run_domains": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_int, c_double, c_i64, c_double,
+                                       ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p]),
     "pint_max_reduce": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "pint_equal_flag": (c_int, [c_void_p, c_i32, c_i64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pint_tri1d_plan_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p, c_void_p, c_void_p]),

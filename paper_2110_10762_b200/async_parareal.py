@@ -273,13 +273,18 @@ def audit_device_trace(records: np.ndarray, p: int, counts=None) -> dict:
 def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = None, *,
                               max_events: int = 200_000, delay_frac: float = 0.0,
                               seed: int = 0, record_trace: bool = False,
-                              trace_cap: int | None = None) -> DeviceAsyncResult:
+                              trace_cap: int | None = None, domains: int = 1) -> DeviceAsyncResult:
     """Asynchronous Parareal with real concurrency on the GPU (PAPER.md
     Algorithm 2): one persistent launch; thread-block clusters act as workers
     that claim slice activations, read the freshest published predecessor
     (no waiting, versioned ring buffers) and publish their update. Stops when
     every slice is drained and its last change is below epsilon, or at exact
-    quiescence when epsilon is None."""
+    quiescence when epsilon is None.
+
+    ``domains > 1`` splits the slices into that many contiguous domains with
+    their own rings, mailboxes and status boards, hosted by one launch on this
+    GPU: the multi-GPU protocol of ``distributed.run_async_parareal_distributed``
+    (P2P push of the boundary state, distributed stop) on one device."""
     import time
 
     if p < 1:
@@ -302,12 +307,14 @@ def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = 
     if record_trace:
         cap = int(trace_cap if trace_cap is not None else min(max_events, 1_000_000))
         trace_buf = np.zeros((cap, len(TRACE_FIELDS)), dtype=np.int64)
-    rc = lib.pint_async_run_traced(fine.handle, coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
-                                   float(-1.0 if epsilon is None else epsilon), int(max_events), float(delay_frac),
-                                   int(seed), ctypes.c_void_p(out.data_ptr()), counts.ctypes.data_as(ctypes.c_void_p),
-                                   info.ctypes.data_as(ctypes.c_void_p),
-                                   ctypes.c_void_p(trace_buf.ctypes.data if trace_buf is not None else 0), cap,
-                                   ctypes.c_void_p(_device.stream_ptr(fine.device)))
+    if not 1 <= int(domains) <= p:
+        raise ValueError(f"need 1 <= domains <= p, got {domains}")
+    rc = lib.pint_async_run_domains(fine.handle, coarse.handle, ctypes.c_void_p(lam.data_ptr()), int(p),
+                                    int(domains), float(-1.0 if epsilon is None else epsilon), int(max_events),
+                                    float(delay_frac), int(seed), ctypes.c_void_p(out.data_ptr()),
+                                    counts.ctypes.data_as(ctypes.c_void_p), info.ctypes.data_as(ctypes.c_void_p),
+                                    ctypes.c_void_p(trace_buf.ctypes.data if trace_buf is not None else 0), cap,
+                                    ctypes.c_void_p(_device.stream_ptr(fine.device)))
     _native.check(rc, fine._ctx.handle, "pint_async_run")
     wall = time.perf_counter() - t0
     if info[2]:

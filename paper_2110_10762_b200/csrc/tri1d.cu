@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "pint_internal.cuh"
+#include "tri1d_device.cuh"
 
 namespace cg = cooperative_groups;
 typedef long double ld;
@@ -258,378 +259,6 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
   return P;
 }
 
-// ============================================================ device side
-
-template <int CH>
-struct Tri1DParams {
-  ChunkFactors<CH> reg, tail;
-  const double *table;  // [NF][T]
-  int64_t N;
-  int64_t steps;
-  double E;
-  double f_first, f_last;
-  int T, nW, tb;
-  int t_last, l_last;
-  int has_forcing;
-};
-
-#define FULLMASK 0xffffffffu
-
-__device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(FULLMASK, v, d); }
-__device__ __forceinline__ double shfl_down_d(double v, int d) { return __shfl_down_sync(FULLMASK, v, d); }
-__device__ __forceinline__ double shfl_d(double v, int l) { return __shfl_sync(FULLMASK, v, l); }
-
-// Trapezoidal rule: raw state x, forward multiplies by q inline.
-template <int CH>
-__device__ __forceinline__ double chunk_forward_raw(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
-  double y0 = F.w[0 + z] * x[0];
-  x[0] = F.q[0 + z] * x[0];
-#pragma unroll
-  for (int j = 1; j < CH - 1; ++j) {
-    y0 = fma(F.w[j + z], x[j], y0);
-    x[j] = fma(F.e[j + z], x[j - 1], F.q[j + z] * x[j]);
-  }
-  return y0;
-}
-
-template <int CH>
-__device__ __forceinline__ void chunk_back_raw(double (&x)[CH], const ChunkFactors<CH> &F, double s_left, int z) {
-#pragma unroll
-  for (int j = CH - 2; j >= 0; --j) x[j] = fma(F.e[j + z], x[j + 1], fma(F.h[j + z], s_left, x[j]));
-}
-
-// Backward Euler: chunk slots carry the pivot-scaled state t_j = q_j x_j
-// between steps (the scaling multiply is issued in the back-substitution,
-// where it is off the critical path and needs no extra registers); the
-// forward elimination is then d'_j = t_j + e_j d'_{j-1}, one FMA per point.
-template <int CH>
-__device__ __forceinline__ void chunk_scale(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
-#pragma unroll
-  for (int j = 0; j < CH - 1; ++j) x[j] = F.q[j + z] * x[j];
-}
-
-template <int CH>
-__device__ __forceinline__ double chunk_forward_scaled(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
-  double y0 = F.ws[0 + z] * x[0];
-#pragma unroll
-  for (int j = 1; j < CH - 1; ++j) {
-    y0 = fma(F.ws[j + z], x[j], y0);
-    x[j] = fma(F.e[j + z], x[j - 1], x[j]);
-  }
-  return y0;
-}
-
-template <int CH, bool OUT_RAW>
-__device__ __forceinline__ void chunk_back_scaled(double (&x)[CH], const ChunkFactors<CH> &F, double s_left, int z) {
-  double xn = x[CH - 1];
-#pragma unroll
-  for (int j = CH - 2; j >= 0; --j) {
-    const double xr = fma(F.e[j + z], xn, fma(F.h[j + z], s_left, x[j]));
-    x[j] = OUT_RAW ? xr : F.q[j + z] * xr;
-    xn = xr;
-  }
-}
-
-struct StepCtx {
-  uint32_t tab;   // shared address: this thread's table row (NF doubles)
-  int TB;
-  uint32_t gbuf;  // shared address: gather [2][4][nW+1] doubles
-  uint32_t mbar;  // shared address: two mbarriers (one per gather parity)
-  int nW;
-  int t, lane, Wg;
-  int CL;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-// Volatile shared loads: the per-thread tables are re-read every step instead
-// of being hoisted into (spilled) registers across the step loop.
-__device__ __forceinline__ double lds(uint32_t a) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
-// Non-volatile shared load: free to be scheduled (and CSE'd) within a step;
-// its address comes from opaque() once per step so it is never hoisted out of
-// the step loop into (spilled) registers.
-__device__ __forceinline__ double lds_free(uint32_t a) {
-  double v;
-  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t opaque(uint32_t x) {
-  uint32_t y;
-  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
-               :: "r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}"
-      :: "r"(bar), "r"(parity) : "memory");
-}
-
-// Publish this warp's level-2 values to every CTA of the cluster and wait for
-// the whole slice's values of step `sc` (double buffered by sc & 1; the
-// mbarrier of each buffer completes one phase per use).
-template <int NV>
-__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double v0, double v1, double v2,
-                                                    double v3) {
-  const uint32_t par = sc & 1u;
-  const uint32_t stride = (uint32_t)(c.nW + 1);
-  const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
-  const uint32_t bar = c.mbar + par * 8u;
-  if (c.lane < c.CL) {
-    const uint32_t rgb = mapa(gb, (uint32_t)c.lane);
-    const uint32_t rbar = mapa(bar, (uint32_t)c.lane);
-    const uint32_t o = (uint32_t)c.Wg * 8u;
-    st_async_f64(rgb + o, v0, rbar);
-    st_async_f64(rgb + stride * 8u + o, v1, rbar);
-    st_async_f64(rgb + 2u * stride * 8u + o, v2, rbar);
-    if (NV == 4) st_async_f64(rgb + 3u * stride * 8u + o, v3, rbar);
-  }
-  if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * NV * 8u);
-  mbar_wait_parity(bar, (sc >> 1) & 1u);
-  return gb;
-}
-
-#define TAB(f) lds_free(tab + (uint32_t)(f) * 8u)
-
-#ifdef PINT_PHASE_TIMING
-// debug build only (scripts/phase_timing.py): clock64 stamps of one step per warp
-__device__ long long *g_phase_buf;
-__device__ int g_phase_step;
-#define PHASE(id)                                                                                         \
-  if (g_phase_buf && sc == (uint32_t)g_phase_step && (c.lane == 0)) {                                    \
-    g_phase_buf[((size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))) * 8 + (id)] = clock64(); \
-  }
-#else
-#define PHASE(id)
-#endif
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// One implicit step on the register-resident chunk. `extra_in` (warp-uniform)
-// is published through the gather and its max over all warps of the slice is
-// returned in *extra_out when WITH_EXTRA. Backward Euler: IN_RAW means the
-// chunk slots hold the raw state (else the pivot-scaled one), OUT_RAW asks for
-// a raw result (else scaled for the next step). The separator is always raw.
-template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
-__device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
-                                         uint32_t sc, double extra_in, double *extra_out) {
-  const bool regular = !GENERAL || c.t < P.tb;
-  const uint32_t tab = opaque(c.tab);
-  // A uniform, step-variant zero (step counters stay below 2^31, checked on
-  // the host): indexing the chunk factors with it keeps them in the constant
-  // bank, loaded straight into uniform registers (LDCU) for each DFMA every
-  // step, instead of being hoisted into general registers and moved back
-  // (R2UR) before every use: -13 % per step at C2.
-  const int z = (int)(sc >> 31);
-  PHASE(0)
-  double xo[CN ? CH : 1];
-  if (CN) {
-#pragma unroll
-    for (int j = 0; j < CH; ++j) xo[j] = x[j];
-  } else if (IN_RAW) {
-    if (regular) chunk_scale<CH>(x, P.reg, z);
-    else chunk_scale<CH>(x, P.tail, z);
-  }
-  if (GENERAL && P.has_forcing) {
-    if (c.t == 0) x[0] += P.f_first;
-    if (c.t == P.t_last) {
-#pragma unroll
-      for (int j = 0; j < CH; ++j)
-        if (j == P.l_last) x[j] += P.f_last;
-    }
-  }
-  double y0;
-  if (CN) {
-    if (regular) y0 = chunk_forward_raw<CH>(x, P.reg, z);
-    else y0 = chunk_forward_raw<CH>(x, P.tail, z);
-  } else {
-    if (regular) y0 = chunk_forward_scaled<CH>(x, P.reg, z);
-    else y0 = chunk_forward_scaled<CH>(x, P.tail, z);
-  }
-  PHASE(1)
-  const double ylast = x[CH - 2];
-  const double dsep = x[CH - 1];
-  double y0n = shfl_down_d(y0, 1);
-  if (c.lane == 31) y0n = 0.0;
-  double b = TAB(TF_MASK) * (dsep - P.E * (ylast + y0n));
-#pragma unroll
-  for (int r = 0; r < 5; ++r) {
-    const int d = 1 << r;
-    const double bm = shfl_up_d(b, d);
-    const double bp = shfl_down_d(b, d);
-    b = fma(-TAB(TF_PCR_G + r), bp, fma(-TAB(TF_PCR_A + r), bm, b));
-  }
-  PHASE(2)
-  const double y1 = b * TAB(TF_PCR_INV);
-  const double y1_30 = shfl_d(y1, 30);
-  const double pw = fma(-TAB(TF_CP), y1_30, b);
-  const double gP = shfl_d(pw, 31);
-  const double gQ = shfl_d(y1, 0);
-  const double gZ = shfl_d(y0, 0);
-  PHASE(3)
-  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in));
-  PHASE(4)
-  const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
-  double sl = 0.0, sr = 0.0, ex = 0.0;
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int V = c.lane + 32 * j;
-    double B = 0.0;
-    if (V < c.nW) {
-      const uint32_t o = (uint32_t)V * 8u;
-      B = fma(-TAB(TF_R2 + 3 * J + j), lds_free(gb + stride8 + o + 8u),
-              fma(-TAB(TF_R2 + 2 * J + j), lds_free(gb + 2u * stride8 + o + 8u), lds_free(gb + o)));
-      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 3u * stride8 + o));
-    }
-    sl = fma(TAB(TF_R2 + j), B, sl);
-    sr = fma(TAB(TF_R2 + J + j), B, sr);
-  }
-  // split butterfly: the lower half-warp reduces sl, the upper half sr
-  {
-    const bool lo = c.lane < 16;
-    double keep = lo ? sl : sr;
-    keep += __shfl_xor_sync(FULLMASK, lo ? sr : sl, 16);
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) keep += __shfl_xor_sync(FULLMASK, keep, o);
-    sl = __shfl_sync(FULLMASK, keep, 0);
-    sr = __shfl_sync(FULLMASK, keep, 16);
-  }
-  if (WITH_EXTRA) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) ex = fmax(ex, __shfl_xor_sync(FULLMASK, ex, o));
-  }
-  if (WITH_EXTRA) *extra_out = ex;
-  double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
-  if (c.lane == 31) s = sr;
-  double s_left = shfl_up_d(s, 1);
-  if (c.lane == 0) s_left = sl;
-  PHASE(5)
-  x[CH - 1] = s;
-  if (CN) {
-    if (regular) chunk_back_raw<CH>(x, P.reg, s_left, z);
-    else chunk_back_raw<CH>(x, P.tail, s_left, z);
-  } else {
-    if (regular) chunk_back_scaled<CH, OUT_RAW>(x, P.reg, s_left, z);
-    else chunk_back_scaled<CH, OUT_RAW>(x, P.tail, s_left, z);
-  }
-  if (CN) {
-#pragma unroll
-    for (int j = 0; j < CH; ++j) x[j] = fma(2.0, x[j], -xo[j]);
-  }
-  PHASE(6)
-}
-
-// Shared-memory setup common to all kernels. Ends with a cluster barrier so
-// the mbarriers and zeroed gather buffers are initialised cluster-wide before
-// any remote store.
-template <int CH, int J>
-__device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *smem, int rank) {
-  StepCtx c;
-  c.TB = blockDim.x;
-  c.CL = P.T / c.TB;
-  c.nW = P.nW;
-  c.t = rank * c.TB + threadIdx.x;
-  c.lane = threadIdx.x & 31;
-  c.Wg = c.t >> 5;
-  const int NF = 15 + 4 * J;  // odd: the per-thread rows are bank-conflict free
-  double *tab = smem;
-  for (int f = 0; f < NF; ++f) tab[threadIdx.x * NF + f] = P.table[(size_t)f * P.T + c.t];
-  c.tab = smem_u32(tab + threadIdx.x * NF);
-  double *gbuf = smem + NF * c.TB;
-  for (int i = threadIdx.x; i < 8 * (c.nW + 1); i += c.TB) gbuf[i] = 0.0;
-  c.gbuf = smem_u32(gbuf);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 8 * (c.nW + 1));
-  c.mbar = smem_u32(bars);
-  if (threadIdx.x == 0) {
-    mbar_init(c.mbar, 1);
-    mbar_init(c.mbar + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  cg::this_cluster().sync();
-  return c;
-}
-
-// S implicit steps from a raw state to a raw state; the step counter `sc`
-// drives the double-buffered exchange. With extra_out != nullptr the first
-// step also reduces extra_in (max) over the slice.
-template <int CH, int J, bool CN, bool GENERAL>
-__device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
-                                          uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
-  if (S == 1) {
-    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, sc, extra_in, extra_out);
-    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, sc, 0.0, nullptr);
-    ++sc;
-    return;
-  }
-  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, sc, extra_in, extra_out);
-  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, sc, 0.0, nullptr);
-  ++sc;
-  for (int64_t s = 1; s < S - 1; ++s, ++sc) tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, sc, 0.0, nullptr);
-  tri_step<CH, J, CN, GENERAL, false, true, false>(x, P, c, sc, 0.0, nullptr);
-  ++sc;
-}
-
-template <int CH>
-__device__ __forceinline__ void load_chunk(double (&x)[CH], const double *src, int64_t N, int t) {
-  const int64_t base = (int64_t)t * CH;
-  const double *p = src + base;
-  if (base + CH <= N && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-#pragma unroll
-    for (int j = 0; j < CH; j += 2) {
-      double2 v = *reinterpret_cast<const double2 *>(p + j);
-      x[j] = v.x;
-      x[j + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < CH; ++j) x[j] = (base + j < N) ? p[j] : 0.0;
-  }
-}
-
-template <int CH>
-__device__ __forceinline__ void store_chunk(const double (&x)[CH], double *dst, int64_t N, int t) {
-  const int64_t base = (int64_t)t * CH;
-  double *p = dst + base;
-  if (base + CH <= N && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-#pragma unroll
-    for (int j = 0; j < CH; j += 2) *reinterpret_cast<double2 *>(p + j) = make_double2(x[j], x[j + 1]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-      if (base + j < N) p[j] = x[j];
-  }
-}
-
 template <int CH, int J, bool CN, bool GENERAL, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 tri1d_batch_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__restrict__ in,
@@ -666,11 +295,6 @@ tri1d_init_kernel(const __grid_constant__ Tri1DParams<CH> P, double *lam, double
   cluster.sync();
 }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(FULLMASK, v, o));
-  return v;
-}
 
 // One synchronous sweep with the coarse chain fused with the correction
 // (parareal.py:119-127): the running iterate next[i-1] never leaves the SMs.
@@ -813,61 +437,6 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   }
   if (bad) atomicExch(nonfinite, 1);
   cluster.sync();
-}
-
-// ============================================================== launchers
-
-template <int CH>
-static Tri1DParams<CH> make_params(const pint_op *op) {
-  const Tri1DPlan &pl = op->plan;
-  Tri1DParams<CH> P;
-  memset(&P, 0, sizeof(P));
-  for (int j = 0; j < CH; ++j) {
-    P.reg.q[j] = pl.fac_reg[0 * CH + j];
-    P.reg.e[j] = pl.fac_reg[1 * CH + j];
-    P.reg.h[j] = pl.fac_reg[2 * CH + j];
-    P.reg.w[j] = pl.fac_reg[3 * CH + j];
-    P.tail.q[j] = pl.fac_tail[0 * CH + j];
-    P.tail.e[j] = pl.fac_tail[1 * CH + j];
-    P.tail.h[j] = pl.fac_tail[2 * CH + j];
-    P.tail.w[j] = pl.fac_tail[3 * CH + j];
-    P.reg.ws[j] = pl.fac_reg[4 * CH + j];
-    P.tail.ws[j] = pl.fac_tail[4 * CH + j];
-  }
-  P.table = op->d_table;
-  P.N = pl.N;
-  P.steps = pl.steps;
-  P.E = pl.E;
-  P.f_first = pl.cn ? pl.f_first : pl.fq_first;
-  P.f_last = pl.cn ? pl.f_last : pl.fq_last;
-  P.T = pl.T;
-  P.nW = pl.nW;
-  P.tb = pl.tb;
-  P.t_last = pl.t_last;
-  P.l_last = pl.l_last;
-  P.has_forcing = (pl.f_first != 0.0 || pl.f_last != 0.0) ? 1 : 0;
-  return P;
-}
-
-template <typename Kern, typename... Args>
-static void launch_cluster(Kern kern, int grid, int block, int cl, size_t smem, cudaStream_t s,
-                           Args... args) {
-  PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (cl > 8) PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(block, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cl;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PINT_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 static size_t smem_bytes(const Tri1DPlan &pl, int TB) {
@@ -1099,435 +668,3 @@ extern "C" int pint_tri1d_plan_host(const pint_op_desc *d, int32_t *dims_out, do
   }
 }
 
-// ======================================================= asynchronous runtime
-//
-// Asynchronous Parareal with real concurrency (reference semantics:
-// async_parareal.py:24-84, Algorithm 2): one persistent launch whose
-// thread-block clusters repeatedly claim a slice activation from an atomic
-// ticket queue (round-robin order, per-slice try-lock), run
-//     F(remembered) -> read the freshest published predecessor -> G(fresh)
-//     -> new = F-only ? F(rem) : (G(fresh) + F(rem)) - G(rem) -> publish
-// and never wait on another cluster: predecessor states are read from a
-// ring of R version-stamped buffers with a seqlock check (retry if the
-// writer lapped the slot), so no co-residency is required and staleness is
-// whatever the hardware schedule produces. G(rem) is the previous
-// activation's G(fresh) (cached per slice). Termination (checked by the
-// cluster that just published): every slice drained (consumed the newest
-// predecessor version) and every last change < eps, or, with eps < 0, exact
-// quiescence (every slice's last activation was F-only on the newest
-// predecessor version).
-
-struct AsyncArgs {
-  double *ring;            // (P+1) x R x N  published versions
-  double *remb;            // (P+1) x N      remembered predecessor reading
-  double *gremb;           // (P+1) x N      G(remembered)
-  double *scratch;         // nclusters x 2 x N (F result, fresh reading)
-  long long *ver;          // (P+1) newest published version per slice
-  long long *vrem;         // (P+1) version of the remembered reading
-  long long *consumed;     // (P+1) predecessor version consumed at the last activation
-  int *busy;               // (P+1) try-lock
-  int *stable;             // (P+1) last activation was F-only
-  long long *counts;       // (P+1) activations per slice
-  double *last_delta;      // (P+1)
-  unsigned long long *ticket;
-  int *stop;               // 1 = converged, 2 = max_events reached
-  int *nonfinite;
-  long long *events;
-  long long *retries;
-  int64_t P, N;
-  int R;
-  double eps;              // < 0: exact quiescence
-  int64_t max_events;
-  double delay_frac;       // injected delay per activation: U(0, delay_frac) * t_F
-  unsigned long long seed;
-  long long *trace;        // optional: ASYNC_TRACE_FIELDS int64 per published activation, in publish order
-  long long trace_cap;
-};
-
-// trace record: slice, fresh predecessor version read, remembered version,
-// F-only flag, delta (bits), globaltimer at F start / at publish, cluster
-constexpr int ASYNC_TRACE_FIELDS = 8;
-
-__device__ __forceinline__ long long ld_acquire_s64(const long long *p) {
-  long long v;
-  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_s64(long long *p, long long v) {
-  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
-
-// Stop test (async_parareal.py:52-58 / quiescence): every slice drained and
-// every last change < eps (eps >= 0), or every slice stable (eps < 0).
-__device__ bool async_done(const AsyncArgs &A) {
-  for (long long s = 1; s <= A.P; ++s) {
-    const long long vp = (s - 1 == 0) ? 0 : ld_acquire_s64(A.ver + s - 1);
-    if (*(volatile long long *)(A.consumed + s) != vp) return false;
-    if (A.eps >= 0.0 ? !(*(volatile double *)(A.last_delta + s) < A.eps) : !*(volatile int *)(A.stable + s))
-      return false;
-  }
-  return true;
-}
-
-template <int CH>
-__device__ __forceinline__ void load_chunk_cg(double (&x)[CH], const double *src, int64_t N, int t) {
-  const int64_t base = (int64_t)t * CH;
-#pragma unroll
-  for (int j = 0; j < CH; ++j) x[j] = (base + j < N) ? __ldcg(src + base + j) : 0.0;
-}
-
-// broadcast a few int64 control words from rank 0 / thread 0 to every CTA
-__device__ __forceinline__ void ctl_broadcast(long long *ctl, int CL, int n) {
-  cg::cluster_group cluster = cg::this_cluster();
-  for (int r = 0; r < CL; ++r) {
-    long long *dst = cluster.map_shared_rank(ctl, r);
-    for (int q = 0; q < n; ++q) dst[q] = ctl[q];
-  }
-}
-
-template <int CH, int J, bool CNF, bool CNG, bool GENERAL>
-__global__ void __launch_bounds__(256, 1)
-tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_constant__ Tri1DParams<CH> PG,
-                   const AsyncArgs A) {
-  extern __shared__ double smem[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int TB = blockDim.x;
-  const int NF = 15 + 4 * J;
-  const int nW = PF.nW;
-  // layout: [tabF][tabG][gather 8(nW+1)][2 mbarriers][ctl 8 x int64][red 32]
-  double *tabF = smem;
-  double *tabG = smem + NF * TB;
-  double *gbuf = tabG + NF * TB;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 8 * (nW + 1));
-  long long *ctl = reinterpret_cast<long long *>(bars + 2);
-  double *red = reinterpret_cast<double *>(ctl + 8);
-  StepCtx cF, cG;
-  cF.TB = cG.TB = TB;
-  cF.CL = cG.CL = PF.T / TB;
-  cF.nW = cG.nW = nW;
-  cF.t = cG.t = rank * TB + threadIdx.x;
-  cF.lane = cG.lane = threadIdx.x & 31;
-  cF.Wg = cG.Wg = cF.t >> 5;
-  for (int f = 0; f < NF; ++f) {
-    tabF[threadIdx.x * NF + f] = PF.table[(size_t)f * PF.T + cF.t];
-    tabG[threadIdx.x * NF + f] = PG.table[(size_t)f * PG.T + cF.t];
-  }
-  cF.tab = smem_u32(tabF + threadIdx.x * NF);
-  cG.tab = smem_u32(tabG + threadIdx.x * NF);
-  for (int i = threadIdx.x; i < 8 * (nW + 1); i += TB) gbuf[i] = 0.0;
-  cF.gbuf = cG.gbuf = smem_u32(gbuf);
-  cF.mbar = cG.mbar = smem_u32(bars);
-  if (threadIdx.x == 0) {
-    mbar_init(cF.mbar, 1);
-    mbar_init(cF.mbar + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  cluster.sync();
-
-  const int64_t N = A.N, P = A.P;
-  const int CL = cF.CL;
-  const int64_t cid = blockIdx.x / CL;
-  double *sF = A.scratch + (size_t)cid * 2 * N;
-  double *sFresh = sF + N;
-  const int64_t base = (int64_t)cF.t * CH;
-  uint32_t sc = 0;
-  double x[CH];
-  bool bad = false;
-  for (;;) {
-    // ---- claim an activation (rank 0, thread 0), broadcast to the cluster
-    if (rank == 0 && threadIdx.x == 0) {
-      long long slice = -1;
-      unsigned backoff = 32;
-      for (;;) {
-        if (*(volatile int *)A.stop) break;
-        const unsigned long long tk = atomicAdd(A.ticket, 1ull);
-        if (tk >= (unsigned long long)A.max_events * 64ull) {  // livelock guard
-          atomicCAS(A.stop, 0, 2);
-          break;
-        }
-        const long long i = 1 + (long long)(tk % (unsigned long long)P);
-        if (atomicCAS(A.busy + i, 0, 1) != 0) continue;
-        const long long vp = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
-        if (*(volatile int *)(A.stable + i) && *(volatile long long *)(A.consumed + i) == vp) {
-          // nothing new to consume: an activation would reproduce the same
-          // value, i.e. a zero change; record it as such without publishing
-          *(volatile double *)(A.last_delta + i) = 0.0;
-          __threadfence();
-          atomicExch(A.busy + i, 0);
-          if (async_done(A)) atomicExch(A.stop, 1);
-          __nanosleep(backoff);
-          backoff = min(backoff * 2, 4096u);
-          continue;
-        }
-        slice = i;
-        break;
-      }
-      ctl[0] = slice;
-      ctl_broadcast(ctl, CL, 1);
-    }
-    cluster.sync();
-    const long long i = ctl[0];
-    if (i < 0) break;
-
-    // ---- F(remembered)
-    const unsigned long long tf0 = globaltimer();
-    load_chunk_cg<CH>(x, A.remb + i * N, N, cF.t);
-    run_steps<CH, J, CNF, GENERAL>(x, PF, cF, sc, PF.steps, 0.0, nullptr);
-    store_chunk<CH>(x, sF, N, cF.t);
-    if (A.delay_frac > 0.0 && rank == 0 && threadIdx.x == 0) {
-      const unsigned long long tF = globaltimer() - tf0;
-      const unsigned long long h = mix64(A.seed ^ ((unsigned long long)i << 32) ^ (unsigned long long)A.counts[i]);
-      const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
-      const unsigned long long until = globaltimer() + (unsigned long long)(u * A.delay_frac * (double)tF);
-      while (globaltimer() < until) __nanosleep(1000);
-    }
-
-    // ---- freshest predecessor (seqlock read of the ring)
-    long long v = 0;
-    for (int attempt = 0;; ++attempt) {
-      if (rank == 0 && threadIdx.x == 0) {
-        ctl[1] = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
-        ctl_broadcast(ctl + 1, CL, 1);
-      }
-      cluster.sync();
-      v = ctl[1];
-      load_chunk_cg<CH>(x, A.ring + ((size_t)(i - 1) * A.R + (size_t)(v % A.R)) * N, N, cF.t);
-      __syncthreads();
-      if (rank == 0 && threadIdx.x == 0) {
-        const long long v2 = (i - 1 == 0) ? 0 : ld_acquire_s64(A.ver + i - 1);
-        ctl[2] = (v2 <= v + A.R - 2) ? 1 : 0;
-        if (!ctl[2]) atomicAdd((unsigned long long *)A.retries, 1ull);
-        ctl_broadcast(ctl + 2, CL, 1);
-      }
-      cluster.sync();
-      if (ctl[2]) break;
-    }
-    const long long vr = A.vrem[i];
-    // bitwise comparison with the remembered reading (array_equal semantics)
-    double mism = 0.0;
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-      if (base + j < N && !(x[j] == __ldcg(A.remb + i * N + base + j))) mism = 1.0;
-    mism = warp_max(mism);
-    store_chunk<CH>(x, sFresh, N, cF.t);
-
-    // ---- G(fresh), with the mismatch flag reduced over the slice on the way
-    double anymism = 0.0;
-    run_steps<CH, J, CNG, GENERAL>(x, PG, cG, sc, PG.steps, mism, &anymism);
-    const bool fonly = (v == vr) || (anymism == 0.0);
-
-    // ---- correction, delta, publish into the next ring slot
-    const long long vi = A.ver[i];
-    const double *cur = A.ring + ((size_t)i * A.R + (size_t)(vi % A.R)) * N + base;
-    double *dst = A.ring + ((size_t)i * A.R + (size_t)((vi + 1) % A.R)) * N + base;
-    double *gw = A.gremb + i * N + base;
-    double *rw = A.remb + i * N + base;
-    double dm = 0.0;
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      if (base + j < N) {
-        const double g = x[j];
-        const double f = __ldcg(sF + base + j);
-        const double nv = fonly ? f : (g + f) - __ldcg(gw + j);
-        dm = fmax(dm, fabs(nv - __ldcg(cur + j)));
-        bad |= !isfinite(nv);
-        dst[j] = nv;
-        gw[j] = g;
-        rw[j] = __ldcg(sFresh + base + j);
-      }
-    }
-    dm = warp_max(dm);
-    __threadfence();
-    if ((threadIdx.x & 31) == 0) cluster.map_shared_rank(red, 0)[cF.Wg] = dm;
-    cluster.sync();
-    if (rank == 0 && threadIdx.x == 0) {
-      double d = 0.0;
-      for (int w = 0; w < nW; ++w) d = fmax(d, red[w]);
-      A.last_delta[i] = d;
-      A.vrem[i] = v;
-      A.consumed[i] = v;
-      A.stable[i] = fonly ? 1 : 0;
-      A.counts[i] += 1;
-      const long long ev = (long long)atomicAdd((unsigned long long *)A.events, 1ull) + 1;
-      if (A.trace && ev - 1 < A.trace_cap) {
-        long long *r = A.trace + (ev - 1) * ASYNC_TRACE_FIELDS;
-        r[0] = i;
-        r[1] = v;
-        r[2] = vr;
-        r[3] = fonly ? 1 : 0;
-        r[4] = __double_as_longlong(d);
-        r[5] = (long long)tf0;
-        r[6] = (long long)globaltimer();
-        r[7] = cid;
-      }
-      __threadfence();
-      st_release_s64(A.ver + i, vi + 1);
-      atomicExch(A.busy + i, 0);
-      if (async_done(A)) atomicExch(A.stop, 1);
-      else if (ev >= A.max_events) atomicCAS(A.stop, 0, 2);
-    }
-  }
-  if (bad) atomicExch(A.nonfinite, 1);
-  cluster.sync();
-}
-
-extern "C" int pint_async_run_traced(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
-                                     int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
-                                     int64_t *counts_out, int64_t *info_out, int64_t *trace_out, int64_t trace_cap,
-                                     void *stream) {
-  if (!fine || !coarse) return PINT_EARG;
-  pint_ctx *ctx = fine->ctx;
-  try {
-    if (fine->desc.ndim != 1 || coarse->desc.ndim != 1 || fine->desc.rule == PINT_RULE_FORWARD_EULER ||
-        coarse->desc.rule == PINT_RULE_FORWARD_EULER)
-      pint_throw(PINT_EUNSUPPORTED, "the device async runtime supports 1-D implicit fine and coarse operators");
-    const Tri1DPlan &pf = fine->plan, &pg = coarse->plan;
-    if (pf.N != pg.N || pf.CH != pg.CH || pf.T != pg.T)
-      pint_throw(PINT_EUNSUPPORTED, "fine and coarse operators must share the register layout (same rule family)");
-    if (p < 1 || !lam0 || !final_out) pint_throw(PINT_EARG, "bad arguments");
-    if (trace_cap < 0 || (trace_cap > 0 && !trace_out)) pint_throw(PINT_EARG, "trace buffer missing");
-    if ((max_events > 0 ? max_events : 20000) * (pf.steps + pg.steps) >= (int64_t)1 << 31)
-      pint_throw(PINT_EARG, "max_events * (fine + coarse steps) must stay below 2^31");
-    cudaStream_t s = (cudaStream_t)stream;
-    const int64_t N = pf.N;
-    const int R = 3;
-    const int CL = fine->batch_cluster;
-    const int TB = pf.T / CL;
-    int dev_sms = ctx->num_sms;
-    const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(p, dev_sms / CL));
-    // device workspace
-    size_t bytes = 0;
-    auto take = [&](size_t n) { size_t o = bytes; bytes += (n + 255) / 256 * 256; return o; };
-    const size_t o_ring = take(sizeof(double) * (p + 1) * R * N), o_remb = take(sizeof(double) * (p + 1) * N),
-                 o_gremb = take(sizeof(double) * (p + 1) * N), o_scr = take(sizeof(double) * ncl * 2 * N),
-                 o_ver = take(8 * (p + 1)), o_vrem = take(8 * (p + 1)), o_cons = take(8 * (p + 1)),
-                 o_busy = take(4 * (p + 1)), o_stab = take(4 * (p + 1)), o_cnt = take(8 * (p + 1)),
-                 o_ld = take(8 * (p + 1)), o_misc = take(64),
-                 o_trace = take(sizeof(long long) * ASYNC_TRACE_FIELDS * (size_t)trace_cap);
-    char *w = nullptr;
-    PINT_CUDA(cudaMallocAsync((void **)&w, bytes, s));
-    PINT_CUDA(cudaMemsetAsync(w + o_ver, 0, o_misc + 64 - o_ver, s));
-    AsyncArgs A;
-    A.ring = (double *)(w + o_ring);
-    A.remb = (double *)(w + o_remb);
-    A.gremb = (double *)(w + o_gremb);
-    A.scratch = (double *)(w + o_scr);
-    A.ver = (long long *)(w + o_ver);
-    A.vrem = (long long *)(w + o_vrem);
-    A.consumed = (long long *)(w + o_cons);
-    A.busy = (int *)(w + o_busy);
-    A.stable = (int *)(w + o_stab);
-    A.counts = (long long *)(w + o_cnt);
-    A.last_delta = (double *)(w + o_ld);
-    A.ticket = (unsigned long long *)(w + o_misc);
-    A.stop = (int *)(w + o_misc + 8);
-    A.nonfinite = (int *)(w + o_misc + 12);
-    A.events = (long long *)(w + o_misc + 16);
-    A.retries = (long long *)(w + o_misc + 24);
-    A.P = p;
-    A.N = N;
-    A.R = R;
-    A.eps = epsilon;
-    A.max_events = max_events > 0 ? max_events : 20000;
-    A.delay_frac = delay_frac;
-    A.seed = seed;
-    A.trace = trace_cap > 0 ? (long long *)(w + o_trace) : nullptr;
-    A.trace_cap = trace_cap;
-    // initial versions: ring[i][0] = lam0[i]; remembered = lam0[i-1] (version 0);
-    // G(remembered) = G(lam0[i-1]) = lam0[i] (coarse initial iterate)
-    const double *L = (const double *)lam0;
-    for (int64_t i = 0; i <= p; ++i)
-      PINT_CUDA(cudaMemcpyAsync(A.ring + (size_t)i * R * N, L + i * N, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-    PINT_CUDA(cudaMemcpyAsync(A.remb + N, L, sizeof(double) * p * N, cudaMemcpyDeviceToDevice, s));
-    PINT_CUDA(cudaMemcpyAsync(A.gremb + N, L + N, sizeof(double) * p * N, cudaMemcpyDeviceToDevice, s));
-    {
-      std::vector<double> inf(p + 1, INFINITY);
-      inf[0] = 0.0;
-      std::vector<long long> minus1(p + 1, -1);
-      PINT_CUDA(cudaMemcpyAsync(A.last_delta, inf.data(), 8 * (p + 1), cudaMemcpyHostToDevice, s));
-      PINT_CUDA(cudaMemcpyAsync(A.consumed, minus1.data(), 8 * (p + 1), cudaMemcpyHostToDevice, s));
-      PINT_CUDA(cudaStreamSynchronize(s));
-    }
-    const size_t sm = sizeof(double) * (2 * (size_t)tri1d_nfields(pf.J) * TB + 8 * (size_t)(pf.nW + 1)) + 16 +
-                      64 + 32 * 8 * 4;
-    const bool general = pf.tb < pf.T || pf.f_first != 0.0 || pf.f_last != 0.0 || pg.f_first != 0.0 ||
-                         pg.f_last != 0.0;
-#define PINT_ASYNC_LAUNCH(CHV, JV, CNF, CNG, GV)                                                        \
-  launch_cluster(tri1d_async_kernel<CHV, JV, CNF, CNG, GV>, (int)(ncl * CL), TB, CL, sm, s,              \
-                 make_params<CHV>(fine), make_params<CHV>(coarse), A)
-#define PINT_ASYNC_J(CHV, CNF, CNG, GV)                      \
-  switch (pf.J) {                                            \
-    case 1: PINT_ASYNC_LAUNCH(CHV, 1, CNF, CNG, GV); break;  \
-    case 2: PINT_ASYNC_LAUNCH(CHV, 2, CNF, CNG, GV); break;  \
-    default: PINT_ASYNC_LAUNCH(CHV, 4, CNF, CNG, GV); break; \
-  }
-    if (pf.CH == 16) {
-      if (pf.cn && pg.cn) {
-        if (general) { PINT_ASYNC_J(16, true, true, true) } else { PINT_ASYNC_J(16, true, true, false) }
-      } else if (pf.cn) {
-        if (general) { PINT_ASYNC_J(16, true, false, true) } else { PINT_ASYNC_J(16, true, false, false) }
-      } else if (!pg.cn) {
-        if (general) { PINT_ASYNC_J(16, false, false, true) } else { PINT_ASYNC_J(16, false, false, false) }
-      } else {
-        pint_throw(PINT_EUNSUPPORTED, "backward-Euler fine with trapezoidal coarse is not fused in the device runtime");
-      }
-    } else {
-      if (general) { PINT_ASYNC_J(32, false, false, true) } else { PINT_ASYNC_J(32, false, false, false) }
-    }
-#undef PINT_ASYNC_J
-#undef PINT_ASYNC_LAUNCH
-    // gather the newest published version of every slice
-    std::vector<long long> ver(p + 1), cnt(p + 1);
-    long long misc[4];
-    int flags[2];
-    PINT_CUDA(cudaMemcpyAsync(ver.data(), A.ver, 8 * (p + 1), cudaMemcpyDeviceToHost, s));
-    PINT_CUDA(cudaMemcpyAsync(cnt.data(), A.counts, 8 * (p + 1), cudaMemcpyDeviceToHost, s));
-    PINT_CUDA(cudaMemcpyAsync(flags, A.stop, 8, cudaMemcpyDeviceToHost, s));
-    PINT_CUDA(cudaMemcpyAsync(misc, A.events, 16, cudaMemcpyDeviceToHost, s));
-    PINT_CUDA(cudaStreamSynchronize(s));
-    if (trace_cap > 0) {
-      const size_t nrec = (size_t)std::min<long long>(misc[0], trace_cap);
-      PINT_CUDA(cudaMemcpyAsync(trace_out, A.trace, sizeof(long long) * ASYNC_TRACE_FIELDS * nrec,
-                                cudaMemcpyDeviceToHost, s));
-    }
-    for (int64_t i = 0; i <= p; ++i)
-      PINT_CUDA(cudaMemcpyAsync((double *)final_out + i * N, A.ring + ((size_t)i * R + (size_t)(ver[i] % R)) * N,
-                                sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-    PINT_CUDA(cudaFreeAsync(w, s));
-    PINT_CUDA(cudaStreamSynchronize(s));
-    if (counts_out)
-      for (int64_t i = 0; i <= p; ++i) counts_out[i] = cnt[i];
-    if (info_out) {
-      info_out[0] = misc[0];   // events (activations)
-      info_out[1] = flags[0];  // 1 converged, 2 max_events
-      info_out[2] = flags[1];  // non-finite
-      info_out[3] = misc[1];   // seqlock retries
-      info_out[4] = ncl;       // concurrent clusters
-    }
-    return PINT_OK;
-  } catch (const PintError &e) {
-    ctx->last_error = e.msg;
-    ctx->last_value = e.value;
-    return e.code;
-  }
-}
-
-extern "C" int pint_async_run(pint_op *fine, pint_op *coarse, const void *lam0, int64_t p, double epsilon,
-                              int64_t max_events, double delay_frac, uint64_t seed, void *final_out,
-                              int64_t *counts_out, int64_t *info_out, void *stream) {
-  return pint_async_run_traced(fine, coarse, lam0, p, epsilon, max_events, delay_frac, seed, final_out, counts_out,
-                               info_out, nullptr, 0, stream);
-}

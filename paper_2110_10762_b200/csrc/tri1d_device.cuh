@@ -1,0 +1,447 @@
+// Device-side building blocks of the 1-D implicit propagators, shared by the
+// batched/sweep kernels (tri1d.cu) and the asynchronous runtime (async_rt.cu).
+// See tri1d.cu for the algorithm (three-level partitioned tridiagonal solve).
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "pint_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+// ============================================================ device side
+
+template <int CH>
+struct Tri1DParams {
+  ChunkFactors<CH> reg, tail;
+  const double *table;  // [NF][T]
+  int64_t N;
+  int64_t steps;
+  double E;
+  double f_first, f_last;
+  int T, nW, tb;
+  int t_last, l_last;
+  int has_forcing;
+};
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(FULLMASK, v, d); }
+__device__ __forceinline__ double shfl_down_d(double v, int d) { return __shfl_down_sync(FULLMASK, v, d); }
+__device__ __forceinline__ double shfl_d(double v, int l) { return __shfl_sync(FULLMASK, v, l); }
+
+// Trapezoidal rule: raw state x, forward multiplies by q inline.
+template <int CH>
+__device__ __forceinline__ double chunk_forward_raw(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
+  double y0 = F.w[0 + z] * x[0];
+  x[0] = F.q[0 + z] * x[0];
+#pragma unroll
+  for (int j = 1; j < CH - 1; ++j) {
+    y0 = fma(F.w[j + z], x[j], y0);
+    x[j] = fma(F.e[j + z], x[j - 1], F.q[j + z] * x[j]);
+  }
+  return y0;
+}
+
+template <int CH>
+__device__ __forceinline__ void chunk_back_raw(double (&x)[CH], const ChunkFactors<CH> &F, double s_left, int z) {
+#pragma unroll
+  for (int j = CH - 2; j >= 0; --j) x[j] = fma(F.e[j + z], x[j + 1], fma(F.h[j + z], s_left, x[j]));
+}
+
+// Backward Euler: chunk slots carry the pivot-scaled state t_j = q_j x_j
+// between steps (the scaling multiply is issued in the back-substitution,
+// where it is off the critical path and needs no extra registers); the
+// forward elimination is then d'_j = t_j + e_j d'_{j-1}, one FMA per point.
+template <int CH>
+__device__ __forceinline__ void chunk_scale(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
+#pragma unroll
+  for (int j = 0; j < CH - 1; ++j) x[j] = F.q[j + z] * x[j];
+}
+
+template <int CH>
+__device__ __forceinline__ double chunk_forward_scaled(double (&x)[CH], const ChunkFactors<CH> &F, int z) {
+  double y0 = F.ws[0 + z] * x[0];
+#pragma unroll
+  for (int j = 1; j < CH - 1; ++j) {
+    y0 = fma(F.ws[j + z], x[j], y0);
+    x[j] = fma(F.e[j + z], x[j - 1], x[j]);
+  }
+  return y0;
+}
+
+template <int CH, bool OUT_RAW>
+__device__ __forceinline__ void chunk_back_scaled(double (&x)[CH], const ChunkFactors<CH> &F, double s_left, int z) {
+  double xn = x[CH - 1];
+#pragma unroll
+  for (int j = CH - 2; j >= 0; --j) {
+    const double xr = fma(F.e[j + z], xn, fma(F.h[j + z], s_left, x[j]));
+    x[j] = OUT_RAW ? xr : F.q[j + z] * xr;
+    xn = xr;
+  }
+}
+
+struct StepCtx {
+  uint32_t tab;   // shared address: this thread's table row (NF doubles)
+  int TB;
+  uint32_t gbuf;  // shared address: gather [2][4][nW+1] doubles
+  uint32_t mbar;  // shared address: two mbarriers (one per gather parity)
+  int nW;
+  int t, lane, Wg;
+  int CL;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Volatile shared loads: the per-thread tables are re-read every step instead
+// of being hoisted into (spilled) registers across the step loop.
+__device__ __forceinline__ double lds(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// Non-volatile shared load: free to be scheduled (and CSE'd) within a step;
+// its address comes from opaque() once per step so it is never hoisted out of
+// the step loop into (spilled) registers.
+__device__ __forceinline__ double lds_free(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :: "r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}"
+      :: "r"(bar), "r"(parity) : "memory");
+}
+
+// Publish this warp's level-2 values to every CTA of the cluster and wait for
+// the whole slice's values of step `sc` (double buffered by sc & 1; the
+// mbarrier of each buffer completes one phase per use).
+template <int NV>
+__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double v0, double v1, double v2,
+                                                    double v3) {
+  const uint32_t par = sc & 1u;
+  const uint32_t stride = (uint32_t)(c.nW + 1);
+  const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
+  const uint32_t bar = c.mbar + par * 8u;
+  if (c.lane < c.CL) {
+    const uint32_t rgb = mapa(gb, (uint32_t)c.lane);
+    const uint32_t rbar = mapa(bar, (uint32_t)c.lane);
+    const uint32_t o = (uint32_t)c.Wg * 8u;
+    st_async_f64(rgb + o, v0, rbar);
+    st_async_f64(rgb + stride * 8u + o, v1, rbar);
+    st_async_f64(rgb + 2u * stride * 8u + o, v2, rbar);
+    if (NV == 4) st_async_f64(rgb + 3u * stride * 8u + o, v3, rbar);
+  }
+  if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * NV * 8u);
+  mbar_wait_parity(bar, (sc >> 1) & 1u);
+  return gb;
+}
+
+#define TAB(f) lds_free(tab + (uint32_t)(f) * 8u)
+
+#ifdef PINT_PHASE_TIMING
+// debug build only (scripts/phase_timing.py): clock64 stamps of one step per warp
+static __device__ long long *g_phase_buf;
+static __device__ int g_phase_step;
+#define PHASE(id)                                                                                         \
+  if (g_phase_buf && sc == (uint32_t)g_phase_step && (c.lane == 0)) {                                    \
+    g_phase_buf[((size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))) * 8 + (id)] = clock64(); \
+  }
+#else
+#define PHASE(id)
+#endif
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One implicit step on the register-resident chunk. `extra_in` (warp-uniform)
+// is published through the gather and its max over all warps of the slice is
+// returned in *extra_out when WITH_EXTRA. Backward Euler: IN_RAW means the
+// chunk slots hold the raw state (else the pivot-scaled one), OUT_RAW asks for
+// a raw result (else scaled for the next step). The separator is always raw.
+template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
+__device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
+                                         uint32_t sc, double extra_in, double *extra_out) {
+  const bool regular = !GENERAL || c.t < P.tb;
+  const uint32_t tab = opaque(c.tab);
+  // A uniform, step-variant zero (step counters stay below 2^31, checked on
+  // the host): indexing the chunk factors with it keeps them in the constant
+  // bank, loaded straight into uniform registers (LDCU) for each DFMA every
+  // step, instead of being hoisted into general registers and moved back
+  // (R2UR) before every use: -13 % per step at C2.
+  const int z = (int)(sc >> 31);
+  PHASE(0)
+  double xo[CN ? CH : 1];
+  if (CN) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) xo[j] = x[j];
+  } else if (IN_RAW) {
+    if (regular) chunk_scale<CH>(x, P.reg, z);
+    else chunk_scale<CH>(x, P.tail, z);
+  }
+  if (GENERAL && P.has_forcing) {
+    if (c.t == 0) x[0] += P.f_first;
+    if (c.t == P.t_last) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j)
+        if (j == P.l_last) x[j] += P.f_last;
+    }
+  }
+  double y0;
+  if (CN) {
+    if (regular) y0 = chunk_forward_raw<CH>(x, P.reg, z);
+    else y0 = chunk_forward_raw<CH>(x, P.tail, z);
+  } else {
+    if (regular) y0 = chunk_forward_scaled<CH>(x, P.reg, z);
+    else y0 = chunk_forward_scaled<CH>(x, P.tail, z);
+  }
+  PHASE(1)
+  const double ylast = x[CH - 2];
+  const double dsep = x[CH - 1];
+  double y0n = shfl_down_d(y0, 1);
+  if (c.lane == 31) y0n = 0.0;
+  double b = TAB(TF_MASK) * (dsep - P.E * (ylast + y0n));
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int d = 1 << r;
+    const double bm = shfl_up_d(b, d);
+    const double bp = shfl_down_d(b, d);
+    b = fma(-TAB(TF_PCR_G + r), bp, fma(-TAB(TF_PCR_A + r), bm, b));
+  }
+  PHASE(2)
+  const double y1 = b * TAB(TF_PCR_INV);
+  const double y1_30 = shfl_d(y1, 30);
+  const double pw = fma(-TAB(TF_CP), y1_30, b);
+  const double gP = shfl_d(pw, 31);
+  const double gQ = shfl_d(y1, 0);
+  const double gZ = shfl_d(y0, 0);
+  PHASE(3)
+  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in));
+  PHASE(4)
+  const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
+  double sl = 0.0, sr = 0.0, ex = 0.0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int V = c.lane + 32 * j;
+    double B = 0.0;
+    if (V < c.nW) {
+      const uint32_t o = (uint32_t)V * 8u;
+      B = fma(-TAB(TF_R2 + 3 * J + j), lds_free(gb + stride8 + o + 8u),
+              fma(-TAB(TF_R2 + 2 * J + j), lds_free(gb + 2u * stride8 + o + 8u), lds_free(gb + o)));
+      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 3u * stride8 + o));
+    }
+    sl = fma(TAB(TF_R2 + j), B, sl);
+    sr = fma(TAB(TF_R2 + J + j), B, sr);
+  }
+  // split butterfly: the lower half-warp reduces sl, the upper half sr
+  {
+    const bool lo = c.lane < 16;
+    double keep = lo ? sl : sr;
+    keep += __shfl_xor_sync(FULLMASK, lo ? sr : sl, 16);
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) keep += __shfl_xor_sync(FULLMASK, keep, o);
+    sl = __shfl_sync(FULLMASK, keep, 0);
+    sr = __shfl_sync(FULLMASK, keep, 16);
+  }
+  if (WITH_EXTRA) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ex = fmax(ex, __shfl_xor_sync(FULLMASK, ex, o));
+  }
+  if (WITH_EXTRA) *extra_out = ex;
+  double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
+  if (c.lane == 31) s = sr;
+  double s_left = shfl_up_d(s, 1);
+  if (c.lane == 0) s_left = sl;
+  PHASE(5)
+  x[CH - 1] = s;
+  if (CN) {
+    if (regular) chunk_back_raw<CH>(x, P.reg, s_left, z);
+    else chunk_back_raw<CH>(x, P.tail, s_left, z);
+  } else {
+    if (regular) chunk_back_scaled<CH, OUT_RAW>(x, P.reg, s_left, z);
+    else chunk_back_scaled<CH, OUT_RAW>(x, P.tail, s_left, z);
+  }
+  if (CN) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) x[j] = fma(2.0, x[j], -xo[j]);
+  }
+  PHASE(6)
+}
+
+// Shared-memory setup common to all kernels. Ends with a cluster barrier so
+// the mbarriers and zeroed gather buffers are initialised cluster-wide before
+// any remote store.
+template <int CH, int J>
+__device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *smem, int rank) {
+  StepCtx c;
+  c.TB = blockDim.x;
+  c.CL = P.T / c.TB;
+  c.nW = P.nW;
+  c.t = rank * c.TB + threadIdx.x;
+  c.lane = threadIdx.x & 31;
+  c.Wg = c.t >> 5;
+  const int NF = 15 + 4 * J;  // odd: the per-thread rows are bank-conflict free
+  double *tab = smem;
+  for (int f = 0; f < NF; ++f) tab[threadIdx.x * NF + f] = P.table[(size_t)f * P.T + c.t];
+  c.tab = smem_u32(tab + threadIdx.x * NF);
+  double *gbuf = smem + NF * c.TB;
+  for (int i = threadIdx.x; i < 8 * (c.nW + 1); i += c.TB) gbuf[i] = 0.0;
+  c.gbuf = smem_u32(gbuf);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbuf + 8 * (c.nW + 1));
+  c.mbar = smem_u32(bars);
+  if (threadIdx.x == 0) {
+    mbar_init(c.mbar, 1);
+    mbar_init(c.mbar + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cg::this_cluster().sync();
+  return c;
+}
+
+// S implicit steps from a raw state to a raw state; the step counter `sc`
+// drives the double-buffered exchange. With extra_out != nullptr the first
+// step also reduces extra_in (max) over the slice.
+template <int CH, int J, bool CN, bool GENERAL>
+__device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
+                                          uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
+  if (S == 1) {
+    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, sc, extra_in, extra_out);
+    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, sc, 0.0, nullptr);
+    ++sc;
+    return;
+  }
+  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, sc, extra_in, extra_out);
+  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, sc, 0.0, nullptr);
+  ++sc;
+  for (int64_t s = 1; s < S - 1; ++s, ++sc) tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, sc, 0.0, nullptr);
+  tri_step<CH, J, CN, GENERAL, false, true, false>(x, P, c, sc, 0.0, nullptr);
+  ++sc;
+}
+
+template <int CH>
+__device__ __forceinline__ void load_chunk(double (&x)[CH], const double *src, int64_t N, int t) {
+  const int64_t base = (int64_t)t * CH;
+  const double *p = src + base;
+  if (base + CH <= N && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+    for (int j = 0; j < CH; j += 2) {
+      double2 v = *reinterpret_cast<const double2 *>(p + j);
+      x[j] = v.x;
+      x[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) x[j] = (base + j < N) ? p[j] : 0.0;
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ void store_chunk(const double (&x)[CH], double *dst, int64_t N, int t) {
+  const int64_t base = (int64_t)t * CH;
+  double *p = dst + base;
+  if (base + CH <= N && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+    for (int j = 0; j < CH; j += 2) *reinterpret_cast<double2 *>(p + j) = make_double2(x[j], x[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (base + j < N) p[j] = x[j];
+  }
+}
+
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(FULLMASK, v, o));
+  return v;
+}
+
+// ============================================================== launchers
+
+template <int CH>
+static Tri1DParams<CH> make_params(const pint_op *op) {
+  const Tri1DPlan &pl = op->plan;
+  Tri1DParams<CH> P;
+  memset(&P, 0, sizeof(P));
+  for (int j = 0; j < CH; ++j) {
+    P.reg.q[j] = pl.fac_reg[0 * CH + j];
+    P.reg.e[j] = pl.fac_reg[1 * CH + j];
+    P.reg.h[j] = pl.fac_reg[2 * CH + j];
+    P.reg.w[j] = pl.fac_reg[3 * CH + j];
+    P.tail.q[j] = pl.fac_tail[0 * CH + j];
+    P.tail.e[j] = pl.fac_tail[1 * CH + j];
+    P.tail.h[j] = pl.fac_tail[2 * CH + j];
+    P.tail.w[j] = pl.fac_tail[3 * CH + j];
+    P.reg.ws[j] = pl.fac_reg[4 * CH + j];
+    P.tail.ws[j] = pl.fac_tail[4 * CH + j];
+  }
+  P.table = op->d_table;
+  P.N = pl.N;
+  P.steps = pl.steps;
+  P.E = pl.E;
+  P.f_first = pl.cn ? pl.f_first : pl.fq_first;
+  P.f_last = pl.cn ? pl.f_last : pl.fq_last;
+  P.T = pl.T;
+  P.nW = pl.nW;
+  P.tb = pl.tb;
+  P.t_last = pl.t_last;
+  P.l_last = pl.l_last;
+  P.has_forcing = (pl.f_first != 0.0 || pl.f_last != 0.0) ? 1 : 0;
+  return P;
+}
+
+template <typename Kern, typename... Args>
+static void launch_cluster(Kern kern, int grid, int block, int cl, size_t smem, cudaStream_t s,
+                           Args... args) {
+  PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (cl > 8) PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PINT_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+

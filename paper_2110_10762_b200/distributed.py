@@ -175,3 +175,184 @@ def run_parareal_sharded(coarse, fine, u0, p_local: int, epsilon: float, k_max: 
             stop = "k_max"
             break
     return {"k_final": k, "stop_reason": stop, "deltas": deltas, "shard": sh.prev.clone()}
+
+
+# ================================================= asynchronous, across GPUs
+def async_partition(p: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous slice ranges (lo, hi), 1-based inclusive, one per rank —
+    the same split the C runtime uses (async_rt.cu, pint_async_run_domains)."""
+    if world < 1 or p < world:
+        raise ValueError(f"need 1 <= world <= p, got world={world}, p={p}")
+    return [(1 + p * r // world, p * (r + 1) // world) for r in range(world)]
+
+
+class NativeAsyncDomain:
+    """One rank's domain of the device async runtime (include/pint_abi.h,
+    pint_async_domain_*): a workspace with the rank's version rings, a ghost
+    mailbox for the predecessor slice and a status board, exported to the
+    peers as a CUDA IPC handle. The kernel pushes the rank's last slice into
+    the next rank's mailbox with P2P stores (async_rt.cu)."""
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, coarse, fine, p: int, lo: int, hi: int, world: int, index: int, trace_cap: int = 0):
+        import ctypes
+
+        from . import _native
+        self._ct = ctypes
+        self.lib = _native.load_library()
+        self._native = _native
+        self.fine, self.coarse = fine, coarse
+        self.ctx = fine._ctx.handle
+        self.lo, self.hi, self.nloc = lo, hi, hi - lo + 1
+        self.trace_cap = int(trace_cap)
+        h = ctypes.c_void_p()
+        rc = self.lib.pint_async_domain_create(fine.handle, coarse.handle, int(p), int(lo), int(hi), int(world),
+                                               int(index), 0, self.trace_cap, ctypes.byref(h))
+        _native.check(rc, self.ctx, "pint_async_domain_create")
+        self.handle = h
+
+    def ipc_handle(self) -> bytes:
+        buf = (self._ct.c_ubyte * self.HANDLE_BYTES)()
+        rc = self.lib.pint_async_domain_ipc_handle(self.handle, buf)
+        self._native.check(rc, self.ctx, "pint_async_domain_ipc_handle")
+        return bytes(buf)
+
+    def connect(self, handles: list[bytes], nloc_all: list[int]) -> None:
+        import numpy as np
+        blob = b"".join(handles)
+        arr = (self._ct.c_ubyte * len(blob)).from_buffer_copy(blob)
+        nl = np.asarray(nloc_all, dtype=np.int64)
+        rc = self.lib.pint_async_domain_connect(self.handle, arr, nl.ctypes.data_as(self._ct.c_void_p))
+        self._native.check(rc, self.ctx, "pint_async_domain_connect")
+
+    def reset(self, rows: torch.Tensor) -> None:
+        from . import _device
+        rc = self.lib.pint_async_domain_reset(self.handle, self._ct.c_void_p(rows.data_ptr()),
+                                              self._ct.c_void_p(_device.stream_ptr(self.fine.device)))
+        self._native.check(rc, self.ctx, "pint_async_domain_reset")
+
+    def launch(self, epsilon: float, max_events: int, delay_frac: float, seed: int) -> None:
+        from . import _device
+        arr = (self._ct.c_void_p * 1)(self.handle.value)
+        rc = self.lib.pint_async_domain_launch(1, arr, float(epsilon), int(max_events), float(delay_frac),
+                                               int(seed), self._ct.c_void_p(_device.stream_ptr(self.fine.device)))
+        self._native.check(rc, self.ctx, "pint_async_domain_launch")
+
+    def synchronize(self) -> None:
+        torch.cuda.synchronize(self.fine.device)
+
+    def collect(self, rows_out: torch.Tensor):
+        import numpy as np
+
+        from . import _device
+        counts = np.zeros(self.nloc + 1, dtype=np.int64)
+        info = np.zeros(6, dtype=np.int64)
+        trace = np.zeros((max(self.trace_cap, 1), 8), dtype=np.int64)
+        rc = self.lib.pint_async_domain_collect(self.handle, self._ct.c_void_p(rows_out.data_ptr()),
+                                                counts.ctypes.data_as(self._ct.c_void_p),
+                                                info.ctypes.data_as(self._ct.c_void_p),
+                                                trace.ctypes.data_as(self._ct.c_void_p), self.trace_cap,
+                                                self._ct.c_void_p(_device.stream_ptr(self.fine.device)))
+        self._native.check(rc, self.ctx, "pint_async_domain_collect")
+        return counts, info, trace[:self.trace_cap]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.pint_async_domain_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | None = None, *,
+                                   max_events: int = 200_000, delay_frac: float = 0.0, seed: int = 0,
+                                   record_trace: bool = False, trace_cap: int | None = None,
+                                   domain_factory=None, coarse_init=None) -> dict:
+    """Asynchronous Parareal over all ranks (Algorithm 2; reference
+    run_async_parareal, async_parareal.py:61-84), one domain of contiguous
+    slices per GPU. The data path is peer memory only: each rank's kernel
+    pushes its last slice into the next rank's mailbox with P2P stores and the
+    stop decision is taken on device from the status boards. NCCL reduces the
+    outcome afterwards (stop code, non-finite flag, activation counts, the
+    trace) and gathers the final iterate.
+
+    Returns {"final": (p+1) x N tensor on this rank's device (every rank),
+    "counts", "activations", "stop_reason", "kappa", "wall_s", "trace"}.
+    ``domain_factory(coarse, fine, p, lo, hi, world, rank, trace_cap)`` and
+    ``coarse_init(coarse, u0, p) -> (p+1) x N tensor`` replace the native
+    pieces (the CPU tests drive the protocol with test doubles)."""
+    import time
+
+    import numpy as np
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if epsilon is not None and epsilon <= 0.0:
+        raise ValueError(f"epsilon must be positive, got {epsilon}")
+    parts = async_partition(p, world)
+    lo, hi = parts[rank]
+    if getattr(fine, "is_tridiagonal", False):
+        from .model import with_register_layout
+        coarse = with_register_layout(coarse, fine.info.points_per_thread)
+    if coarse_init is None:
+        coarse_init = _device_coarse_init
+    lam = coarse_init(coarse, u0, p)  # redundant on every rank: bitwise identical, no exchange
+    dev = lam.device
+    cap = int(trace_cap if trace_cap is not None else min(max_events, 1_000_000)) if record_trace else 0
+    factory = domain_factory or NativeAsyncDomain
+    dom = factory(coarse, fine, p, lo, hi, world, rank, cap)
+    # exchange the workspace handles (host plumbing; 64 bytes per rank)
+    hb = torch.tensor(list(dom.ipc_handle()), dtype=torch.uint8, device=_red_device())
+    allh = [torch.zeros_like(hb) for _ in range(world)]
+    dist.all_gather(allh, hb)
+    handles = [bytes(t.cpu().tolist()) for t in allh]
+    dom.connect(handles, [h_ - l_ + 1 for l_, h_ in parts])
+    dom.reset(lam[lo - 1:hi + 1].contiguous())
+    barrier()  # every mailbox and board is reset before any rank may push
+    t0 = time.perf_counter()
+    dom.launch(-1.0 if epsilon is None else float(epsilon), max_events, delay_frac, seed)
+    dom.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()  # no rank frees its workspace while a peer may still store into it
+    rows = torch.empty(hi - lo + 2, lam.shape[1], dtype=lam.dtype, device=dev)
+    counts, info, trace = dom.collect(rows)
+    barrier()
+    dom.close()
+    # ---- the final convergence reduction (NCCL)
+    red = torch.tensor([float(info[1]), float(info[2]), wall], dtype=torch.float64, device=_red_device())
+    dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    stop_code, nonfinite, wall_max = int(red[0].item()), int(red[1].item()), float(red[2].item())
+    cnt = torch.zeros(p + 1, dtype=torch.int64, device=_red_device())
+    cnt[lo:hi + 1] = torch.as_tensor(counts[1:], device=cnt.device)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    # final iterate: every rank contributes its owned rows (row 0 = u0 from rank 0)
+    full = torch.zeros(p + 1, lam.shape[1], dtype=lam.dtype, device=_red_device())
+    full[lo:hi + 1] = rows[1:].to(full.device)
+    if rank == 0:
+        full[0] = rows[0].to(full.device)
+    dist.all_reduce(full, op=dist.ReduceOp.SUM)
+    tr = None
+    if cap > 0:
+        tt = torch.as_tensor(trace, device=_red_device())
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)  # each record was written by exactly one rank
+        n = min(int(info[0]), cap)
+        tr = tt[:n].cpu().numpy()
+    if nonfinite:
+        raise ValueError("block entries must be finite")
+    counts_all = cnt.cpu().numpy()
+    out = {"final": full.to(dev), "counts": counts_all, "activations": int(info[0]),
+           "stop_reason": {1: "converged", 2: "max_events"}.get(stop_code, "unknown"),
+           "kappa": int(counts_all[1:].max()), "wall_s": wall_max, "trace": tr, "slices": (lo, hi)}
+    return out
+
+
+def _device_coarse_init(coarse, u0, p: int) -> torch.Tensor:
+    from .parareal import _coarse_init_into, _u0_tensor
+    lam = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")
+    lam[0] = _u0_tensor(coarse, u0)
+    _coarse_init_into(coarse, lam, p, None)
+    return lam
