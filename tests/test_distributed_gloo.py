@@ -97,3 +97,116 @@ def test_sharded_run_equals_single_process(tmp_path, world, p_local, eps):
     assert str(got["stop"]) == ref.stop_reason
     assert np.array_equal(got["deltas"], np.array(ref.deltas))
     assert np.array_equal(got["full"], ref.iterates[-1])
+
+
+# ------------------------------------------------ asynchronous, across ranks
+class FakeAsyncDomain:
+    """Test double of distributed.NativeAsyncDomain: checks the handle
+    exchange and the call order, and 'runs' the domain by landing on the
+    exact-quiescence answer (the sequential fine solution),
+    one activation per slice, trace records at global event = slice."""
+
+    calls = []
+
+    def __init__(self, coarse, fine, p, lo, hi, world, rank, cap):
+        self.fine, self.p, self.lo, self.hi, self.world, self.rank, self.cap = fine, p, lo, hi, world, rank, cap
+        self.state = "created"
+
+    def ipc_handle(self):
+        return bytes([self.rank + 1]) * 64
+
+    def connect(self, handles, nloc_all):
+        assert self.state == "created"
+        assert [h for h in handles] == [bytes([x + 1]) * 64 for x in range(self.world)]
+        assert sum(nloc_all) == self.p and nloc_all[self.rank] == self.hi - self.lo + 1
+        self.state = "connected"
+
+    def reset(self, rows):
+        assert self.state == "connected" and rows.shape[0] == self.hi - self.lo + 2
+        self.rows = rows.clone()
+        self.state = "reset"
+
+    def launch(self, eps, max_events, delay, seed):
+        assert self.state == "reset"
+        seq = H.sequential_fine_solve(self.fine, self.u0, self.p)
+        self.result = torch.from_numpy(seq[self.lo - 1:self.hi + 1].copy())
+        self.state = "launched"
+
+    def synchronize(self):
+        pass
+
+    def collect(self, rows_out):
+        assert self.state == "launched"
+        rows_out.copy_(self.result)
+        nloc = self.hi - self.lo + 1
+        counts = np.ones(nloc + 1, dtype=np.int64)
+        counts[0] = 0
+        info = np.array([self.p, 1, 0, 0, 1, nloc], dtype=np.int64)
+        trace = np.zeros((self.cap, 8), dtype=np.int64)
+        for gi in range(self.lo, self.hi + 1):
+            if gi - 1 < self.cap:
+                trace[gi - 1, 0] = gi
+                trace[gi - 1, 3] = 1
+                trace[gi - 1, 7] = self.rank * 65536
+        return counts, info, trace
+
+    def close(self):
+        self.state = "closed"
+
+
+def _async_worker(rank, world, port, p, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_10762_b200 import distributed as D
+    coarse, fine, u0 = problem()
+
+    def factory(*args):
+        d = FakeAsyncDomain(*args)
+        d.u0 = u0
+        return d
+
+    def cinit(c, u, pp):
+        lam = np.zeros((pp + 1, len(u)))
+        lam[0] = u
+        for i in range(1, pp + 1):
+            lam[i] = c.apply(lam[i - 1])
+        return torch.from_numpy(lam)
+
+    res = D.run_async_parareal_distributed(coarse, fine, u0, p, None, record_trace=True, trace_cap=p,
+                                           domain_factory=factory, coarse_init=cinit)
+    np.savez(out + f".{rank}.npz", final=res["final"].numpy(), counts=res["counts"], trace=res["trace"],
+             stop=res["stop_reason"], kappa=res["kappa"], slices=np.array(res["slices"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,p", [(2, 6), (3, 7), (4, 4)])
+def test_async_distributed_protocol(tmp_path, world, p):
+    from paper_2110_10762_b200.distributed import async_partition
+    out = str(tmp_path / "a")
+    mp.start_processes(_async_worker, args=(world, _free_port(), p, out), nprocs=world, join=True,
+                       start_method="spawn")
+    coarse, fine, u0 = problem()
+    seq = H.sequential_fine_solve(fine, u0, p)
+    parts = async_partition(p, world)
+    for r in range(world):
+        got = np.load(out + f".{r}.npz")
+        assert np.array_equal(got["final"], seq)  # every rank holds the assembled iterate
+        assert np.array_equal(got["counts"], np.r_[0, np.ones(p, dtype=np.int64)])
+        assert str(got["stop"]) == "converged" and int(got["kappa"]) == 1
+        assert tuple(got["slices"]) == parts[r]
+        assert np.array_equal(got["trace"][:, 0], np.arange(1, p + 1))  # merged from all ranks
+        owners = got["trace"][:, 7] // 65536
+        assert all(parts[o][0] <= i <= parts[o][1] for o, i in zip(owners, got["trace"][:, 0]))
+
+
+def test_async_partition_matches_the_device_split():
+    from paper_2110_10762_b200.distributed import async_partition
+    for p in range(1, 40):
+        for w in range(1, min(p, 9) + 1):
+            parts = async_partition(p, w)
+            assert parts[0][0] == 1 and parts[-1][1] == p
+            assert all(parts[i][1] + 1 == parts[i + 1][0] for i in range(w - 1))
+            sizes = [h - l + 1 for l, h in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        async_partition(3, 4)

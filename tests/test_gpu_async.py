@@ -167,3 +167,66 @@ def test_device_async_trace_audit(gpu, delay, n, p):
     assert tr.to_jsonl().count("\n") == res.activations
     _, kappa = gpu.update_counts(tr)
     assert kappa == res.kappa
+
+
+# ------------------------------------- multi-domain runtime (multi-GPU protocol)
+def _c1_pair(gpu, n, p):
+    from oracle import heat_oracle as H
+    u0 = H.sine_u0_1d(n, 8, 0)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    return u0, gpu.backward_euler_propagator(ivp, 1 / p, 100), gpu.backward_euler_propagator(ivp, 1 / p, 1)
+
+
+@pytest.mark.parametrize("domains,delay,n,p", [(2, 0.0, 1024, 16), (3, 0.2, 1024, 16), (4, 0.0, 1024, 17),
+                                               (8, 0.1, 1024, 16), (4, 0.0, 65536, 24)])
+def test_device_async_domains_quiescence(gpu, domains, delay, n, p):
+    """Slices split into `domains` contiguous domains with their own rings,
+    ghost mailboxes (the predecessor domain pushes its last slice into them)
+    and status boards, hosted by one launch: the multi-GPU protocol on one
+    device. Exact quiescence must land on the sequential fine solution
+    bitwise, the trace must pass the race audit, and every domain boundary
+    must have carried pushed versions."""
+    from paper_2110_10762_b200.distributed import async_partition
+    u0, fine, coarse = _c1_pair(gpu, n, p)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, delay_frac=delay, seed=11, record_trace=True,
+                                        domains=domains)
+    assert res.stop_reason == "converged"
+    assert np.array_equal(res.final.data, seq)
+    rec = res.trace_records
+    assert len(rec) == res.activations
+    audit = gpu.audit_device_trace(rec, p, res.per_component_counts)
+    assert audit["ok"], audit
+    owners = rec[:, 7] // 65536
+    parts = async_partition(p, domains)
+    assert set(owners.tolist()) == set(range(domains))
+    for o, i in zip(owners, rec[:, 0]):
+        assert parts[o][0] <= i <= parts[o][1]
+    for lo, _ in parts[1:]:
+        first = rec[rec[:, 0] == lo]
+        assert first[:, 1].max() >= 1  # read versions of the ghost pushed by the previous domain
+    last = {}
+    for r in rec:
+        last[int(r[0])] = r
+    assert all(int(last[i][3]) == 1 for i in range(1, p + 1))
+
+
+def test_device_async_domains_epsilon_stop(gpu):
+    n, p = 1024, 16
+    u0, fine, coarse = _c1_pair(gpu, n, p)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    for domains in (2, 4):
+        res = gpu.run_async_parareal_device(coarse, fine, u0, p, 1e-10, domains=domains, seed=domains)
+        assert res.stop_reason == "converged"
+        assert np.max(np.abs(res.final.data - seq)) < 1e-8
+        sync = gpu.run_parareal(coarse, fine, u0, p, 1e-10)
+        assert res.kappa >= sync.k_final
+
+
+def test_device_async_domains_arguments(gpu):
+    n, p = 1024, 4
+    u0, fine, coarse = _c1_pair(gpu, n, p)
+    with pytest.raises(ValueError):
+        gpu.run_async_parareal_device(coarse, fine, u0, p, None, domains=5)
+    with pytest.raises(ValueError):  # the status word holds 21-bit counters
+        gpu.run_async_parareal_device(coarse, fine, u0, p, None, domains=2, max_events=1 << 22)
