@@ -211,6 +211,7 @@ def run_ours(args, rank: int, world: int) -> None:
 
     import paper_2110_10762_b200 as pb
     from paper_2110_10762_b200 import distributed as dist_rt
+    from paper_2110_10762_b200.inputs import sine_u0_1d
     from paper_2110_10762_b200.parareal import SyncEngine
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
@@ -220,8 +221,7 @@ def run_ours(args, rank: int, world: int) -> None:
     ivp = pb.heat1d_system(N_POINTS, 1.0, 0.0, 0.0, 0.0, T_FINAL)
     fine = pb.backward_euler_propagator(ivp, span, FINE_STEPS)
     coarse = pb.backward_euler_propagator(ivp, span, COARSE_STEPS)
-    from oracle import heat_oracle as H  # input generation only (seeded u0)
-    u0 = H.sine_u0_1d(N_POINTS, N_MODES, 0)
+    u0 = sine_u0_1d(N_POINTS, N_MODES, 0)  # seeded synthetic input
 
     if world > 1:
         eng = dist_rt.ShardedSyncEngine(coarse, fine, P_LOCAL, rank, world)

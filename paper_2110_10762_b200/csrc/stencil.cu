@@ -177,6 +177,10 @@ template <typename T>
 void fe2d_wave_apply(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride, cudaStream_t st);
 template <typename T>
 void fe3d_wave_apply(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride, cudaStream_t st);
+template <typename T>
+bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride,
+                     cudaStream_t st);
+int fe3d_tile_default(int esz);
 
 void stencil_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch, int64_t stride, cudaStream_t s) {
   const int64_t S = op->desc.steps;
@@ -186,7 +190,13 @@ void stencil_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
   const bool v1 = getenv("PINT_STENCIL_V1") && atoi(getenv("PINT_STENCIL_V1"));
   const bool wave2 = nd == 2 && !v1, wave3 = nd == 3 && !v1;
   if (wave2) sblk = 8;
-  if (wave3) sblk = 4;
+  int v3 = 0;
+  if (wave3) {
+    // 3-D tiling variant (stencil3d.cu); PINT_FE3D_VARIANT overrides for measurement, 0 = fe3d_wave
+    v3 = fe3d_tile_default(esz);
+    if (const char *e = getenv("PINT_FE3D_VARIANT")) v3 = atoi(e);
+    sblk = v3 > 0 ? 1 : 4;
+  }
   void *scratch = nullptr;
   if (S > sblk) {
     const size_t need = (size_t)nbatch * stride * esz;
@@ -198,6 +208,15 @@ void stencil_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch,
       op->cg_work_bytes = need;
     }
     scratch = op->cg_work;
+  }
+  if (wave3 && v3 > 0) {
+    const bool ok = op->desc.dtype == PINT_F64
+                        ? fe3d_tile_apply<double>(v3, op, (const double *)in, (double *)out, (double *)scratch,
+                                                  nbatch, stride, s)
+                        : fe3d_tile_apply<float>(v3, op, (const float *)in, (float *)out, (float *)scratch, nbatch,
+                                                 stride, s);
+    if (!ok) pint_throw(PINT_EARG, "unknown PINT_FE3D_VARIANT");
+    return;
   }
   if (wave3) {
     if (op->desc.dtype == PINT_F64)

@@ -17,7 +17,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2110_10762_b200 as pb  # noqa: E402
-from oracle import heat_oracle as H  # noqa: E402  (input generation only)
+from paper_2110_10762_b200 import inputs as H  # noqa: E402  (seeded synthetic inputs)
 
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0

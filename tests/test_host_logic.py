@@ -142,3 +142,20 @@ def test_plan_reports_singular_steps():
     d.span, d.steps, d.a_diag = 1.0, 1, 1.0  # u' = u, dt = 1: 1 - dt*a = 0
     dims = (ctypes.c_int32 * 6)()
     assert nat.load_library().pint_tri1d_plan_host(ctypes.byref(d), dims, None, None, None) == nat.PINT_ESINGULAR
+
+
+def test_package_inputs_match_the_oracle_bitwise():
+    """bench.py and the CLI build their seeded inputs with the package
+    (paper_2110_10762_b200/inputs.py), never with oracle/; both must give the
+    same bits as the oracle's generators."""
+    import numpy as np
+
+    from oracle import heat_oracle as H
+    from paper_2110_10762_b200 import inputs as I
+    for n, m, seed in [(1024, 8, 0), (65536, 32, 0), (7, 3, 4)]:
+        assert np.array_equal(I.sine_u0_1d(n, m, seed), H.sine_u0_1d(n, m, seed))
+    assert I.modes_2d() == H.modes_2d() and I.modes_3d() == H.modes_3d()
+    for shape in [(24, 24), (9, 10, 11)]:
+        modes = I.modes_2d() if len(shape) == 2 else I.modes_3d()
+        assert np.array_equal(I.sine_u0_nd(shape, modes, 2), H.sine_u0_nd(shape, modes, 2))
+        assert np.array_equal(I.sine_u0(shape, seed=2), H.sine_u0_nd(shape, modes, 2).reshape(-1))
