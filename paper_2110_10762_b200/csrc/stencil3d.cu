@@ -372,7 +372,7 @@ void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, 
 //         8 = S3 64x48 (NW16 RPT3), 9 = S4 64x36 (NW12 RPT3), 10 = S3 64x40 (NW20 RPT2), 11 = S4 64x40 (NW20 RPT2)
 //   fp64: 1 = S4 64x16, 2 = S3 64x24, 3 = S3 64x20, 4 = S4 64x32 (NW16 RPT2), 5 = S3 64x32 (NW16 RPT2),
 //         6 = S2 64x32 (NW16 RPT2), 7 = S3 64x40 (NW20 RPT2)
-// Defaults measured at the C4 shape (profiles/r02_fe3d_variants.jsonl).
+// Defaults measured at the C4 shape (profiles/r01_fe3d_variants.jsonl).
 int fe3d_tile_default(int esz) { return esz == 4 ? 8 : 5; }
 
 template <typename T>
