@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "pint_internal.cuh"
 
@@ -29,11 +31,26 @@ constexpr int W2 = BX2 + 2 * SMAX2;      // loaded columns per tile
 constexpr int WT2 = W2 / CPT2;           // threads per CTA (136)
 constexpr int YC2 = 128;                 // output rows per chunk
 
-template <typename T, int S>
-__global__ void __launch_bounds__(WT2)
+template <typename T, int S, bool UNROLL, int MINB>
+__global__ void __launch_bounds__(WT2, MINB)
 fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, T r) {
-  __shared__ T sm[2][S][W2 + 2];
   const int tid = threadIdx.x;
+  // fp64: the edge columns of every thread in two planes (a thread's first /
+  // last column), so a warp's neighbour loads and edge stores are contiguous
+  // (no two-way bank conflicts from the CPT2 column stride; C3 fp64 778 -> 817
+  // GPt/s). fp32: interleaved row (the split layout measured 7 % slower).
+  constexpr bool SPLIT = sizeof(T) == 8;
+  __shared__ T sm[2][S][2][WT2 + 2];
+  auto st_edge = [&](int pr, int L, const T (&vv)[CPT2]) {
+    if constexpr (SPLIT) {
+      sm[pr][L][0][1 + tid] = vv[0];
+      sm[pr][L][1][1 + tid] = vv[CPT2 - 1];
+    } else {
+      T *row = &sm[pr][L][0][0];
+#pragma unroll
+      for (int c = 0; c < CPT2; ++c) row[1 + CPT2 * tid + c] = vv[c];
+    }
+  };
   const int x0 = blockIdx.x * BX2 - S;  // first loaded column (halo S)
   const int y0 = blockIdx.y * YC2;
   const T *src = in + (int64_t)blockIdx.z * stride;
@@ -46,7 +63,7 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
     const int lc = CPT2 * tid + c;  // local column
     colout[c] = colin[c] && lc >= S && lc < S + BX2;
   }
-  for (int i = tid; i < 2 * S * (W2 + 2); i += WT2) (&sm[0][0][0])[i] = T(0);
+  for (int i = tid; i < 2 * S * 2 * (WT2 + 2); i += WT2) (&sm[0][0][0][0])[i] = T(0);
   T cur[S][CPT2], prv[S][CPT2], pp[S][CPT2];
 #pragma unroll
   for (int L = 0; L < S; ++L)
@@ -55,7 +72,6 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   __syncthreads();
   const T four = T(4);
   const int ys = y0 - S, ye = min(y0 + YC2, ny) - 1 + S;
-  int par = 0;
   // input rows are prefetched one iteration ahead (the load latency would
   // otherwise sit in front of every row's barrier)
   T pre[CPT2];
@@ -64,7 +80,11 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
 #pragma unroll
     for (int c = 0; c < CPT2; ++c) pre[c] = (rowin && colin[c]) ? __ldg(src + (int64_t)ys * nx + cx + c) : T(0);
   }
-  for (int yy = ys; yy <= ye; ++yy, par ^= 1) {
+  // one row of the wavefront; PAR = shared-buffer parity, EDGE = some level's
+  // row may lie outside the domain
+  auto row = [&](auto par_c, auto edge_c, int yy) {
+    constexpr int par = decltype(par_c)::value;
+    constexpr bool EDGE = decltype(edge_c)::value;
     // level 0: the input row yy
 #pragma unroll
     for (int c = 0; c < CPT2; ++c) cur[0][c] = pre[c];
@@ -74,15 +94,15 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
 #pragma unroll
       for (int c = 0; c < CPT2; ++c) pre[c] = (rowin && colin[c]) ? __ldg(src + (int64_t)yn * nx + cx + c) : T(0);
     }
-#pragma unroll
-    for (int c = 0; c < CPT2; ++c) sm[par][0][1 + CPT2 * tid + c] = cur[0][c];
+    st_edge(par, 0, cur[0]);
     // levels 1..S: level L+1 at row yy-L-1 from level L rows (pp, prv, cur)
 #pragma unroll
     for (int L = 0; L < S; ++L) {
       const int yr = yy - L - 1;
-      const bool rin = yr >= 0 && yr < ny;
-      const T left = sm[par ^ 1][L][CPT2 * tid];
-      const T right = sm[par ^ 1][L][1 + CPT2 * tid + CPT2];
+      const bool rin = !EDGE || (yr >= 0 && yr < ny);
+      // last column of thread tid-1, first column of thread tid+1
+      const T left = SPLIT ? sm[par ^ 1][L][1][tid] : (&sm[par ^ 1][L][0][0])[CPT2 * tid];
+      const T right = SPLIT ? sm[par ^ 1][L][0][tid + 2] : (&sm[par ^ 1][L][0][0])[1 + CPT2 * tid + CPT2];
       T v[CPT2];
 #pragma unroll
       for (int c = 0; c < CPT2; ++c) {
@@ -94,10 +114,8 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
       }
       if (L + 1 < S) {
 #pragma unroll
-        for (int c = 0; c < CPT2; ++c) {
-          cur[L + 1][c] = v[c];
-          sm[par][L + 1][1 + CPT2 * tid + c] = v[c];
-        }
+        for (int c = 0; c < CPT2; ++c) cur[L + 1][c] = v[c];
+        st_edge(par, L + 1, v);
       } else if (yr >= y0 && yr < y0 + YC2 && rin) {
 #pragma unroll
         for (int c = 0; c < CPT2; ++c)
@@ -112,17 +130,58 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
         prv[L][c] = cur[L][c];
       }
     __syncthreads();
+  };
+  using P0 = std::integral_constant<int, 0>;
+  using P1 = std::integral_constant<int, 1>;
+  using Steady = std::false_type;
+  using Edge = std::true_type;
+  int yy = ys;
+  while (yy <= ye) {
+    if (UNROLL && yy >= S && yy + 5 <= ny && yy + 5 <= ye) {
+      // steady state: six rows per trip (three-row register rotation x two
+      // buffer parities: the rotation is register renaming, not moves)
+      row(P0{}, Steady{}, yy);
+      row(P1{}, Steady{}, yy + 1);
+      row(P0{}, Steady{}, yy + 2);
+      row(P1{}, Steady{}, yy + 3);
+      row(P0{}, Steady{}, yy + 4);
+      row(P1{}, Steady{}, yy + 5);
+      yy += 6;
+    } else {
+      row(P0{}, Edge{}, yy);
+      if (yy + 1 > ye) break;
+      row(P1{}, Edge{}, yy + 1);
+      yy += 2;
+    }
   }
+}
+
+// PINT_FE2D_VARIANT (measurement): 0 = rolled row loop, 1 = six-row steady
+// unroll (no register cap), 2 = six-row unroll capped for 3 CTAs/SM (default:
+// C3 fp64 +7 %, fp32 +10 % over 0, profiles/r01_fe2d_variants.jsonl)
+int fe2d_variant() {
+  const char *e = getenv("PINT_FE2D_VARIANT");
+  return e ? atoi(e) : 2;
+}
+
+template <typename T, int S, bool UNROLL, int MINB>
+void launch2v(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, T r, cudaStream_t st) {
+  const unsigned tx = (unsigned)((nx + BX2 - 1) / BX2), ty = (unsigned)((ny + YC2 - 1) / YC2);
+  for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
+    const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
+    fe2d_wave<T, S, UNROLL, MINB><<<dim3(tx, ty, n), WT2, 0, st>>>(in + b0 * stride, out + b0 * stride, stride, nx,
+                                                                   ny, r);
+  }
+  PINT_CUDA(cudaGetLastError());
 }
 
 template <typename T, int S>
 void launch2(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, T r, cudaStream_t st) {
-  const unsigned tx = (unsigned)((nx + BX2 - 1) / BX2), ty = (unsigned)((ny + YC2 - 1) / YC2);
-  for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
-    const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
-    fe2d_wave<T, S><<<dim3(tx, ty, n), WT2, 0, st>>>(in + b0 * stride, out + b0 * stride, stride, nx, ny, r);
+  switch (fe2d_variant()) {
+    case 1: launch2v<T, S, true, 1>(in, out, nb, stride, nx, ny, r, st); break;
+    case 2: launch2v<T, S, true, 3>(in, out, nb, stride, nx, ny, r, st); break;
+    default: launch2v<T, S, false, 1>(in, out, nb, stride, nx, ny, r, st); break;
   }
-  PINT_CUDA(cudaGetLastError());
 }
 
 template <typename T>

@@ -179,3 +179,26 @@ def test_fe3d_tilings_are_bitwise_identical(gpu, monkeypatch, dtype, variants, s
     ref = H.ExplicitND(shape, h, 0.15 * h * h, steps).apply(x[0].cpu().numpy())
     tol = 1e-5 if dtype == "float32" else 1e-12
     assert np.max(np.abs(y[0] - ref)) <= tol * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("shape,steps", [((300, 300), 29), ((41, 57), 9), ((1024, 1024), 12)])
+def test_fe2d_variants_are_bitwise_identical(gpu, monkeypatch, dtype, shape, steps):
+    """The 2-D wavefront variants (rolled / six-row unrolled steady state)
+    give identical bits, and match the oracle."""
+    import torch
+    n = shape[0]
+    if shape[0] != shape[1]:
+        pytest.skip("square grids only")
+    ivp = gpu.heat2d_system(n, t_final=1.0)
+    h = 1.0 / (n + 1)
+    x = torch.rand(3, ivp.dim, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    outs = []
+    for v in (0, 1, 2):
+        monkeypatch.setenv("PINT_FE2D_VARIANT", str(v))
+        F = gpu.forward_euler_propagator(ivp, steps * 0.2 * h * h, steps, dtype=dtype)
+        outs.append(F.apply_batch(x.to(F.dtype)).clone())
+    assert all(torch.equal(o, outs[0]) for o in outs)
+    ref = H.ExplicitND(shape, h, 0.2 * h * h, steps).apply(x[1].cpu().numpy())
+    tol = 1e-5 if dtype == "float32" else 1e-12
+    assert np.max(np.abs(outs[0][1].double().cpu().numpy() - ref)) <= tol * max(1.0, np.max(np.abs(ref)))
