@@ -287,7 +287,7 @@ def run_ours(args, rank: int, world: int) -> None:
         if world == 1:
             # public host-buffer sweep: per-chunk uploads/downloads overlapped with compute
             eng.prev = eng.lam_b
-            d = eng.sweep_host(1, host_in, host_out)
+            d = eng.sweep_host(1, host_in, host_out, graph=True)
         else:
             eng.lam_a.copy_(host_in, non_blocking=True)
             eng.prev = eng.lam_a

@@ -250,14 +250,31 @@ class SyncEngine:
             a = b + 1
         return out
 
+    def row_ranges(self, k: int) -> list:
+        """Rows of the iterate each chunk's upload carries: a partition of
+        [0, p] (chunk c's F needs rows a_c-1 .. b_c-1; its coarse sweep rows
+        up to b_c)."""
+        out, lo = [], 0
+        chunks = self.chunks(k)
+        for c, (a, b) in enumerate(chunks):
+            hi = self.p if c == len(chunks) - 1 else b
+            out.append((lo, hi))
+            lo = hi + 1
+        return out
+
     def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None,
-              d2h_splits: int = 1) -> None:
+              d2h_splits: int = 1, h2d_splits: int = 1) -> None:
         """Sweep k (device work only, stream-ordered): nxt <- new iterate.
         With several chunks, chunk c's coarse sweep overlaps chunk c+1's F.
-        h2d(c, stream) enqueues chunk c's input upload before its F;
-        d2h(lo, hi, last, stream) enqueues the download of slices [lo, hi]
-        as soon as the coarse sweep has produced them (the last chunk's sweep
-        is split into d2h_splits launches so its download overlaps it)."""
+        With h2d_splits > 1 every chunk's F is split into that many launches
+        on their own streams and the coarse sweep follows part by part, so a
+        part's F starts as soon as its rows are uploaded and its results
+        leave as soon as the chain has passed them.
+        h2d(r0, r1, stream) enqueues the upload of iterate rows [r0, r1]
+        before the F that reads them; d2h(lo, hi, last, stream) enqueues the
+        download of slices [lo, hi] once the coarse sweep has produced them
+        (without F parts, the last chunk's sweep is split into d2h_splits
+        launches so its download overlaps it)."""
         chunks = self.chunks(k)
         if len(chunks) == 1 and h2d is None and d2h is None:
             self.fine_batch(k, fine_done_event)
@@ -275,64 +292,136 @@ class SyncEngine:
         cp.wait_stream(main)
         dn.wait_stream(main)
         fs[1].wait_stream(main)
+        rows = self.row_ranges(k)
+        split_f = h2d is not None and self.pipeline and h2d_splits > 1
+
+        def split(a, b, m):
+            m = max(1, min(int(m), b - a + 1))
+            base, extra = divmod(b - a + 1, m)
+            out = []
+            for q in range(m):
+                e = a + base + (1 if q < extra else 0) - 1
+                out.append((a, e))
+                a = e + 1
+            return out
+
+        parts = [split(a, b, h2d_splits if split_f else 1) for (a, b) in chunks]
+        used = {fs[0], fs[1]}
         f_done = []
         for c, (a, b) in enumerate(chunks):
-            st = fs[c % 2]
-            if h2d is not None:
-                h2d(c, cp)
+            evs = []
+            r0 = rows[c][0]
+            for q, (pa, pb) in enumerate(parts[c]):
+                if split_f:
+                    st = self._sub_stream(q)
+                    if c == 0:
+                        st.wait_stream(main)
+                else:
+                    st = fs[c % 2]
+                used.add(st)
+                if h2d is not None:
+                    r1 = rows[c][1] if q == len(parts[c]) - 1 else pb - 1
+                    h2d(r0, r1, cp)
+                    r0 = r1 + 1
+                    ev = torch.cuda.Event()
+                    ev.record(cp)
+                    st.wait_event(ev)
+                self.fine.apply_ptr(self.prev[pa - 1].data_ptr(), self.fv[pa].data_ptr(), pb - pa + 1, n,
+                                    stream=st.cuda_stream)
                 ev = torch.cuda.Event()
-                ev.record(cp)
-                st.wait_event(ev)
-            self.fine.apply_ptr(self.prev[a - 1].data_ptr(), self.fv[a].data_ptr(), b - a + 1, n,
-                                stream=st.cuda_stream)
-            ev = torch.cuda.Event()
-            ev.record(st)
-            f_done.append(ev)
+                ev.record(st)
+                evs.append(ev)
+            f_done.append(evs)
         if fine_done_event is not None:
-            main.wait_stream(fs[1])
+            for st in used:
+                if st is not main:
+                    main.wait_stream(st)
             fine_done_event.record(main)
         lo = 0
         for c, (a, b) in enumerate(chunks):
-            side.wait_event(f_done[c])
             last = c == len(chunks) - 1
-            parts = max(1, min(int(d2h_splits), b - a + 1)) if (last and d2h is not None) else 1
-            base, extra = divmod(b - a + 1, parts)
-            pa = a
-            for q in range(parts):
-                pb = pa + base + (1 if q < extra else 0) - 1
+            if split_f:
+                pieces = [(pr, [f_done[c][q]]) for q, pr in enumerate(parts[c])]
+            else:
+                m = d2h_splits if (last and d2h is not None) else 1
+                pieces = [(pr, f_done[c] if q == 0 else []) for q, pr in enumerate(split(a, b, m))]
+            for q, ((pa, pb), evs) in enumerate(pieces):
+                for ev in evs:
+                    side.wait_event(ev)
                 self.coarse_sweep(pa, nxt, chain_in=(c > 0 or q > 0), hi=pb, stream=side)
-                if last and q == parts - 1:
+                final = last and q == len(pieces) - 1
+                if final:
                     self.reduce_delta(k, stream=side)
                 if d2h is not None:
                     ev = torch.cuda.Event()
                     ev.record(side)
                     dn.wait_event(ev)
-                    d2h(lo, pb, last and q == parts - 1, dn)
+                    d2h(lo, pb, final, dn)
                     lo = pb + 1
-                pa = pb + 1
-        main.wait_stream(fs[1])
+        for st in used:
+            if st is not main:
+                main.wait_stream(st)
         main.wait_stream(side)
         main.wait_stream(cp)
         main.wait_stream(dn)
         self.prev = nxt
 
-    def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor, d2h_splits: int = 4) -> float:
+    def _sub_stream(self, q: int):
+        """Streams of the first chunk's split F launches (independent, so each
+        part's clusters start as soon as its rows are uploaded)."""
+        subs = getattr(self, "_subs", None)
+        if subs is None:
+            subs = self._subs = []
+        while len(subs) <= q:
+            subs.append(torch.cuda.Stream(device=f"cuda:{self.fine.device}"))
+        return subs[q]
+
+    def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor, d2h_splits: int = 4,
+                   h2d_splits: int = 2, graph: bool = False) -> float:
         """One sweep from host (pinned) buffers: host_prev -> device iterate ->
-        sweep -> host_next. Each chunk's upload overlaps the previous chunk's
-        F; downloads follow the coarse sweep in pieces on their own stream.
-        Returns the delta."""
-        chunks = self.chunks(k)
-        rows = []
-        lo = 0
-        for c, (a, b) in enumerate(chunks):
-            hi = self.p if c == len(chunks) - 1 else b
-            rows.append((lo, hi))
-            lo = hi + 1
+        sweep -> host_next. Uploads run ahead of the F launches that read
+        them; with h2d_splits > 1 each chunk's F runs as that many launches
+        that start as their rows arrive, and the coarse sweep and the
+        downloads follow part by part (C2 on B200: h2d 52 GB/s, d2h 29 GB/s,
+        so the last part's download is the exposed tail; 2 parts measured
+        best, scripts/e2e_probe.py).
+        ``graph=True`` captures the sweep's stream work (copies and launches on
+        all streams) once per buffer pairing into a CUDA graph and replays it,
+        so repeated sweeps cost one graph launch of host time. Returns the delta."""
         dev_prev = self.lam_a if self.prev is not self.lam_a else self.lam_b
         nxt = self.lam_b if dev_prev is self.lam_a else self.lam_a
+        if graph:
+            key = (k, host_prev.data_ptr(), host_next.data_ptr(), d2h_splits, h2d_splits, dev_prev is self.lam_a)
+            graphs = self.__dict__.setdefault("_graphs", {})
+            g = graphs.get(key)
+            if g is None:
+                g = self._capture(lambda: self._host_sweep_work(k, dev_prev, nxt, host_prev, host_next, d2h_splits,
+                                                                h2d_splits))
+                graphs[key] = g
+            g.replay()
+            self.prev = nxt
+        else:
+            self._host_sweep_work(k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits)
+        torch.cuda.current_stream(self.fine.device).synchronize()
+        if self.host[1].item() != 0.0:
+            raise ValueError("block entries must be finite")
+        return float(self.host[0].item())
 
-        def h2d(c, st):
-            r0, r1 = rows[c]
+    def _capture(self, work):
+        """CUDA graph of ``work()`` (stream-ordered work that forks to and
+        joins back from the engine's side streams)."""
+        dev = f"cuda:{self.fine.device}"
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+            work()
+        torch.cuda.current_stream(dev).wait_stream(cap)
+        return g
+
+    def _host_sweep_work(self, k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits) -> None:
+
+        def h2d(r0, r1, st):
             with torch.cuda.stream(st):
                 dev_prev[r0:r1 + 1].copy_(host_prev[r0:r1 + 1], non_blocking=True)
 
@@ -344,24 +433,25 @@ class SyncEngine:
                     self.host[1:2].copy_(self.flag.to(torch.float64), non_blocking=True)
 
         self.prev = dev_prev
-        self.sweep(k, nxt, h2d=h2d, d2h=d2h, d2h_splits=d2h_splits)
-        torch.cuda.current_stream(self.fine.device).synchronize()
-        if self.host[1].item() != 0.0:
-            raise ValueError("block entries must be finite")
-        return float(self.host[0].item())
+        self.sweep(k, nxt, h2d=h2d, d2h=d2h, d2h_splits=d2h_splits, h2d_splits=h2d_splits)
 
     def launches_per_sweep(self, k: int = 1) -> int:
         """Our kernel launches per sweep (fused path: F batch and coarse sweep
         per chunk, max-reduce)."""
         return 2 * len(self.chunks(k)) + 1 if self.fused else 1 + 3 * self.p
 
-    def launches_per_host_sweep(self, k: int = 1, d2h_splits: int = 4) -> int:
-        """As launches_per_sweep, for sweep_host (the last chunk's coarse
-        sweep is split into d2h_splits launches)."""
+    def launches_per_host_sweep(self, k: int = 1, d2h_splits: int = 4, h2d_splits: int = 2) -> int:
+        """As launches_per_sweep, for sweep_host (every chunk's F split into
+        h2d_splits launches with the coarse sweep following part by part;
+        without a pipeline, one F launch and d2h_splits sweep launches)."""
+        if not self.fused:
+            return 1 + 3 * self.p
         ch = self.chunks(k)
+        if self.pipeline and h2d_splits > 1:
+            parts = sum(min(h2d_splits, b - a + 1) for a, b in ch)
+            return 2 * parts + 1
         a, b = ch[-1]
-        # F per chunk + coarse sweep per chunk (the last one split) + max-reduce
-        return 2 * len(ch) + min(d2h_splits, b - a + 1) if self.fused else 1 + 3 * self.p
+        return 2 * len(ch) - 1 + min(d2h_splits, b - a + 1) + 1
 
     def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
         """Coarse chain + correction for coarse operators without a fused

@@ -25,6 +25,9 @@ if __name__ == "__main__":
     for v in (0, 1, 2):
         os.environ["PINT_FE2D_VARIANT"] = str(v)
         F = pb.forward_euler_propagator(ivp, steps * 0.2 * h * h, steps, dtype=dtype)
+        if x is None and os.environ.get("FE2D_SINE"):
+            from paper_2110_10762_b200 import inputs
+            x = torch.tensor(inputs.sine_u0((n, n), seed=0), dtype=F.dtype, device="cuda").repeat(p, 1)
         if x is None:
             x = torch.rand(p, ivp.dim, dtype=F.dtype, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
         y = torch.empty_like(x)

@@ -166,3 +166,10 @@ def test_sweep_host_matches_device_sweep(gpu):
     d = eng.sweep_host(1, host_in, host_out)
     assert d == dwant
     assert torch.equal(host_out, want)
+    # the same sweep captured into a CUDA graph and replayed (both buffer parities)
+    for _ in range(3):
+        eng.gcache.copy_(g0)
+        host_out.zero_()
+        d = eng.sweep_host(1, host_in, host_out, graph=True)
+        assert d == dwant
+        assert torch.equal(host_out, want)
