@@ -12,7 +12,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2110_10762_b200 as pb  # noqa: E402
-from oracle import heat_oracle as H  # noqa: E402
+from paper_2110_10762_b200 import inputs as H  # noqa: E402  (seeded synthetic inputs)
 
 
 def main():

@@ -7,7 +7,7 @@ sys.path.insert(0, ROOT)
 import torch
 import paper_2110_10762_b200 as pb
 from paper_2110_10762_b200.parareal import SyncEngine
-from oracle import heat_oracle as H
+from paper_2110_10762_b200 import inputs as H  # seeded synthetic inputs
 
 what = sys.argv[1] if len(sys.argv) > 1 else "both"
 steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 1000
