@@ -273,7 +273,8 @@ def audit_device_trace(records: np.ndarray, p: int, counts=None) -> dict:
 def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = None, *,
                               max_events: int = 200_000, delay_frac: float = 0.0,
                               seed: int = 0, record_trace: bool = False,
-                              trace_cap: int | None = None, domains: int = 1) -> DeviceAsyncResult:
+                              trace_cap: int | None = None, domains: int = 1,
+                              lanes: int = 4) -> DeviceAsyncResult:
     """Asynchronous Parareal with real concurrency on the GPU (PAPER.md
     Algorithm 2): one persistent launch; thread-block clusters act as workers
     that claim slice activations, read the freshest published predecessor
@@ -284,13 +285,24 @@ def run_async_parareal_device(coarse, fine, u0, p: int, epsilon: float | None = 
     ``domains > 1`` splits the slices into that many contiguous domains with
     their own rings, mailboxes and status boards, hosted by one launch on this
     GPU: the multi-GPU protocol of ``distributed.run_async_parareal_distributed``
-    (P2P push of the boundary state, distributed stop) on one device."""
+    (P2P push of the boundary state, distributed stop) on one device.
+
+    2-D/3-D operators run on ``lanes`` CUDA streams instead (one activation =
+    F, G and the correction of one slice as whole-GPU launches,
+    async_streams.py)."""
     import time
 
     if p < 1:
         raise ValueError(f"need p >= 1 subintervals, got {p}")
     if epsilon is not None and epsilon <= 0.0:
         raise ValueError(f"epsilon must be positive, got {epsilon}")
+    if not (fine.is_tridiagonal and coarse.is_tridiagonal):
+        # 2-D/3-D operators: an activation is a whole-GPU job, orchestrated on
+        # streams (async_streams.py); same stopping rules and result fields
+        from .async_streams import run_async_parareal_streams
+        return run_async_parareal_streams(coarse, fine, u0, p, epsilon, lanes=max(lanes, domains),
+                                          domains=domains, max_events=max_events, delay_frac=delay_frac,
+                                          seed=seed, record_trace=True)
     from .model import with_register_layout
     coarse = with_register_layout(coarse, fine.info.points_per_thread) if fine.is_tridiagonal else coarse
     lam = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")

@@ -230,3 +230,47 @@ def test_device_async_domains_arguments(gpu):
         gpu.run_async_parareal_device(coarse, fine, u0, p, None, domains=5)
     with pytest.raises(ValueError):  # the status word holds 21-bit counters
         gpu.run_async_parareal_device(coarse, fine, u0, p, None, domains=2, max_events=1 << 22)
+
+
+# ------------------------------------------- 2-D/3-D: stream-orchestrated runtime
+def _nd_pair(gpu, shape, p, steps, cfl, dtype="float64"):
+    from paper_2110_10762_b200 import inputs
+    n = shape[0]
+    h = 1.0 / (n + 1)
+    span = steps * cfl * h * h
+    u0 = inputs.sine_u0(shape, seed=1)
+    mk = gpu.heat2d_system if len(shape) == 2 else gpu.heat3d_system
+    ivp = mk(n, t_final=p * span, u0=u0)
+    fine = gpu.forward_euler_propagator(ivp, span, steps, dtype=dtype)
+    coarse = gpu.backward_euler_propagator(ivp, span, 1, dtype=dtype)
+    return u0, fine, coarse
+
+
+@pytest.mark.parametrize("shape,p,lanes,domains,delay", [((48, 48), 8, 3, 1, 0.0), ((48, 48), 9, 4, 3, 0.3),
+                                                         ((20, 20, 20), 6, 2, 2, 0.0)])
+def test_stream_async_quiescence_is_the_sequential_solution(gpu, shape, p, lanes, domains, delay):
+    """2-D/3-D async Parareal on CUDA streams: exact quiescence lands on the
+    sequential fine solution bitwise (finite termination), the trace passes
+    the race audit, and domain boundaries carried pushed versions."""
+    from paper_2110_10762_b200.distributed import async_partition
+    u0, fine, coarse = _nd_pair(gpu, shape, p, 40, 0.2 if len(shape) == 2 else 0.15)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, lanes=lanes, domains=domains,
+                                        delay_frac=delay, seed=3)
+    assert res.stop_reason == "converged"
+    assert np.array_equal(res.final.data, seq)
+    audit = gpu.audit_device_trace(res.trace_records, p, res.per_component_counts)
+    assert audit["ok"], audit
+    rec = res.trace_records
+    for lo, _ in async_partition(p, domains)[1:]:
+        assert rec[rec[:, 0] == lo][:, 1].max() >= 1
+
+
+def test_stream_async_epsilon_stop(gpu):
+    u0, fine, coarse = _nd_pair(gpu, (64, 64), 8, 100, 0.2)
+    seq = gpu.sequential_fine_solve(fine, u0, p=8).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, 8, 1e-10, lanes=4, domains=2)
+    assert res.stop_reason == "converged"
+    assert np.max(np.abs(res.final.data - seq)) < 1e-8
+    sync = gpu.run_parareal(coarse, fine, u0, 8, 1e-10)
+    assert res.kappa >= sync.k_final
