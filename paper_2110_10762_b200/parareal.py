@@ -237,16 +237,20 @@ class SyncEngine:
         _native.check(rc, _ctx(self.fine), "pint_max_reduce")
 
     def chunks(self, k: int) -> list:
-        """Live slices [k, p] split into balanced chunks of at most one wave."""
-        live = self.p - k + 1
-        if not self.pipeline or live <= self.wave:
+        """Live slices [k, p] in chunks of at most one wave. The boundaries are
+        those of the balanced split of [1, p] (only the first chunk shrinks as
+        the frozen prefix grows), so the rows a chunk of sweep k+1 reads were
+        produced by the same chunk of sweep k — what lets sweep k+1's first F
+        start before sweep k's chain has finished (``speculate``)."""
+        if not self.pipeline or self.p <= self.wave:
             return [(k, self.p)]
-        n = -(-live // self.wave)
-        base, extra = divmod(live, n)
-        out, a = [], k
+        n = -(-self.p // self.wave)
+        base, extra = divmod(self.p, n)
+        out, a = [], 1
         for c in range(n):
             b = a + base + (1 if c < extra else 0) - 1
-            out.append((a, b))
+            if b >= k:
+                out.append((max(a, k), b))
             a = b + 1
         return out
 
@@ -263,7 +267,7 @@ class SyncEngine:
         return out
 
     def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None,
-              d2h_splits: int = 1, h2d_splits: int = 1) -> None:
+              d2h_splits: int = 1, h2d_splits: int = 1, speculate: bool = False) -> None:
         """Sweep k (device work only, stream-ordered): nxt <- new iterate.
         With several chunks, chunk c's coarse sweep overlaps chunk c+1's F.
         With h2d_splits > 1 every chunk's F is split into that many launches
@@ -274,9 +278,19 @@ class SyncEngine:
         before the F that reads them; d2h(lo, hi, last, stream) enqueues the
         download of slices [lo, hi] once the coarse sweep has produced them
         (without F parts, the last chunk's sweep is split into d2h_splits
-        launches so its download overlaps it)."""
+        launches so its download overlaps it).
+        speculate: also launch sweep k+1's first-chunk F as soon as this
+        sweep's first chunk has its new values (on its own stream, not joined
+        into the current stream), so it runs while this sweep's chain finishes
+        and the host reads the delta; the next ``sweep(k+1)`` uses it (a
+        stop at k discards it)."""
         chunks = self.chunks(k)
-        if len(chunks) == 1 and h2d is None and d2h is None:
+        spec = getattr(self, "_spec", None)
+        self._spec = None
+        if spec is not None and (spec[0] != k or spec[1] is not self.prev or h2d is not None):
+            spec[2].synchronize()  # stale speculation (not this sweep): let it finish, recompute
+            spec = None
+        if len(chunks) == 1 and h2d is None and d2h is None and spec is None:
             self.fine_batch(k, fine_done_event)
             self.coarse_sweep(k, nxt)
             self.reduce_delta(k)
@@ -311,6 +325,9 @@ class SyncEngine:
         for c, (a, b) in enumerate(chunks):
             evs = []
             r0 = rows[c][0]
+            if c == 0 and spec is not None and spec[3] == (a, b):
+                f_done.append([spec[2]])  # launched by the previous sweep
+                continue
             for q, (pa, pb) in enumerate(parts[c]):
                 if split_f:
                     st = self._sub_stream(q)
@@ -358,6 +375,19 @@ class SyncEngine:
                     dn.wait_event(ev)
                     d2h(lo, pb, final, dn)
                     lo = pb + 1
+            if c == 0 and speculate and len(chunks) > 1 and k < self.p:
+                nk = self.chunks(k + 1)
+                a1, b1 = nk[0]
+                if b1 <= b:  # its inputs nxt[a1-1 .. b1-1] come from this chunk
+                    ev0 = torch.cuda.Event()
+                    ev0.record(side)
+                    sp = self._spec_stream()
+                    sp.wait_event(ev0)
+                    self.fine.apply_ptr(nxt[a1 - 1].data_ptr(), self.fv[a1].data_ptr(), b1 - a1 + 1, n,
+                                        stream=sp.cuda_stream)
+                    evs = torch.cuda.Event()
+                    evs.record(sp)
+                    self._spec = (k + 1, nxt, evs, (a1, b1))
         for st in used:
             if st is not main:
                 main.wait_stream(st)
@@ -365,6 +395,12 @@ class SyncEngine:
         main.wait_stream(cp)
         main.wait_stream(dn)
         self.prev = nxt
+
+    def _spec_stream(self):
+        st = getattr(self, "_spec_st", None)
+        if st is None:
+            st = self._spec_st = torch.cuda.Stream(device=f"cuda:{self.fine.device}")
+        return st
 
     def _sub_stream(self, q: int):
         """Streams of the first chunk's split F launches (independent, so each
@@ -505,7 +541,9 @@ def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = N
         nxt = eng.lam_b if eng.prev is eng.lam_a else eng.lam_a
         if record_iterates:
             nxt.copy_(eng.prev)
-        eng.sweep(k, nxt)
+        # sweep k+1's first F starts while this sweep's chain and the host's
+        # delta read finish (discarded if this sweep stops the iteration)
+        eng.sweep(k, nxt, speculate=k < cap)
         delta = eng.read_delta()
         deltas.append(delta)
         slice_deltas.append(eng.deltas.to("cpu").numpy().copy())

@@ -131,9 +131,11 @@ def test_pipelined_sweep_is_bitwise_the_single_launch_sweep(gpu, wave):
         for e in (ref, eng):
             nxt = e.lam_b if e.prev is e.lam_a else e.lam_a
             nxt.copy_(e.prev)
-            e.sweep(k, nxt)
+            e.sweep(k, nxt, speculate=e is eng)  # eng also pre-launches sweep k+1's first F
             outs.append((nxt.clone(), e.read_delta(), e.deltas.clone(), e.gcache.clone()))
-        assert len(eng.chunks(k)) == -(-(p - k + 1) // wave)
+        ch = eng.chunks(k)
+        assert ch[0][0] == k and ch[-1][1] == p and all(b - a + 1 <= wave for a, b in ch)
+        assert all(ch[i][1] + 1 == ch[i + 1][0] for i in range(len(ch) - 1))
         assert torch.equal(outs[0][0], outs[1][0]), k
         assert outs[0][1] == outs[1][1]
         assert torch.equal(outs[0][2], outs[1][2])
