@@ -515,23 +515,120 @@ class SyncEngine:
         return float(self.dmax.item())
 
 
+class LeanSyncEngine:
+    """Synchronous iteration in place: one iterate, the G(old) cache and a
+    chunk of F results — 2 state copies instead of SyncEngine's 4, for
+    problems whose state fills HBM (C5: 129 slices x 512^3 fp32 = 66 GB per
+    copy; 2 copies fit a 180 GB B200, 4 do not). Same arithmetic as
+    SyncEngine's generic sweep (parareal.py:119-127 semantics): F of a chunk
+    runs from the old values (the chunk-boundary row is saved before the
+    chain overwrites it), the chain then corrects slice by slice into the F
+    row (the correction reads F before writing each element) and copies it
+    into the iterate."""
+
+    def __init__(self, coarse, fine, p: int, chunk: int | None = None):
+        if coarse.dim != fine.dim:
+            from .errors import DimensionError
+            raise DimensionError("coarse and fine propagators differ in dimension")
+        self.coarse, self.fine, self.p = coarse, fine, int(p)
+        dev = f"cuda:{fine.device}"
+        n = fine.dim
+        esz = 8 if fine.dtype == torch.float64 else 4
+        if chunk is None:
+            chunk = max(1, min(self.p, (8 << 30) // max(1, n * esz)))
+        self.chunk = int(chunk)
+        self.lam_a = torch.empty(p + 1, n, dtype=fine.dtype, device=dev)
+        self.lam_b = self.lam_a  # in place: the next iterate overwrites this one
+        self.gcache = torch.zeros_like(self.lam_a)
+        self.fv = torch.empty(self.chunk, n, dtype=fine.dtype, device=dev)
+        self.saved = torch.empty(1, n, dtype=fine.dtype, device=dev)
+        self.g = torch.empty(1, n, dtype=fine.dtype, device=dev)
+        self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
+        self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.fonly = torch.zeros(p + 1, dtype=torch.bool, device=dev)
+        self.prev = self.lam_a
+        self.lib = _native.load_library()
+
+    def init(self, u0) -> None:
+        self.lam_a[0] = _u0_tensor(self.coarse, u0)
+        _coarse_init_into(self.coarse, self.lam_a, self.p, self.gcache)
+        self.flag.zero_()
+
+    def sweep(self, k: int, nxt: torch.Tensor, speculate: bool = False, **_) -> None:
+        lam, n, p = self.lam_a, self.fine.dim, self.p
+        if nxt is not lam:
+            raise ValueError("the lean engine updates its iterate in place")
+        self.deltas.zero_()
+        self.fonly[k] = True  # slice k-1 is frozen: F-only for slice k
+        a = k
+        while a <= p:
+            b = min(p, a + self.chunk - 1)
+            m = b - a + 1
+            # F from the old values: row a-1 is frozen (a == k) or was saved
+            # before the previous chunk's chain overwrote it
+            src0 = lam[a - 1] if a == k else self.saved[0]
+            self.fine.apply_ptr(src0.data_ptr(), self.fv[0].data_ptr(), 1, n)
+            if m > 1:
+                self.fine.apply_ptr(lam[a].data_ptr(), self.fv[1].data_ptr(), m - 1, n)
+            if b < p:
+                self.saved[0].copy_(lam[b])
+            for i in range(a, b + 1):
+                self.coarse.apply_ptr(lam[i - 1].data_ptr(), self.g.data_ptr(), 1, n)
+                if i > k:
+                    torch.eq(self.deltas[i - 1:i], 0.0, out=self.fonly[i:i + 1])
+                row = self.fv[i - a:i - a + 1]
+                correct_into(self.fine, self.g, row, self.gcache[i:i + 1], lam[i:i + 1], row,
+                             self.fonly[i:i + 1], self.deltas[i:i + 1], self.flag, 1)
+                self.gcache[i].copy_(self.g[0])
+                lam[i].copy_(row[0])
+            a = b + 1
+        rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, p + 1,
+                                      ctypes.c_void_p(self.dmax.data_ptr()), _stream(self.fine))
+        _native.check(rc, _ctx(self.fine), "pint_max_reduce")
+        self.prev = lam
+
+    def read_delta(self) -> float:
+        if bool(self.flag.item()):
+            raise ValueError("block entries must be finite")
+        return float(self.dmax.item())
+
+
+def _pick_engine(coarse, fine, p: int, engine: str | None):
+    if engine == "lean":
+        return LeanSyncEngine(coarse, fine, p)
+    if engine in (None, "auto") and not coarse.is_tridiagonal:
+        esz = 8 if fine.dtype == torch.float64 else 4
+        need = 4 * (p + 1) * fine.dim * esz
+        free, _ = torch.cuda.mem_get_info(fine.device)
+        if need > 0.8 * free:
+            return LeanSyncEngine(coarse, fine, p)
+    return SyncEngine(coarse, fine, p)
+
+
 def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = None, *,
-                 record_iterates: bool | None = None) -> SyncTrace:
+                 record_iterates: bool | None = None, engine: str | None = None) -> SyncTrace:
     """Iterate from the coarse initialization until a stop condition fires
     (parareal.py:99-138): "threshold" when the sweep-to-sweep change drops
     strictly below epsilon, "exact" at k == p, "k_max" at the budget.
-    Components i < k are frozen (already exact)."""
+    Components i < k are frozen (already exact). ``engine="lean"`` (chosen
+    automatically when four state copies would not fit in HBM) updates one
+    iterate in place (LeanSyncEngine)."""
     if epsilon < 0.0:
         raise ValueError(f"epsilon must be nonnegative, got {epsilon}")
     cap = p if k_max is None else min(int(k_max), p)
     if cap < 1:
         raise ValueError(f"iteration budget must allow k >= 1, got k_max={k_max}")
-    eng = SyncEngine(coarse, fine, p)
+    eng = _pick_engine(coarse, fine, p, engine)
     eng.init(u0)
     esz = 8 if fine.dtype == torch.float64 else 4
     if record_iterates is None:
         record_iterates = (cap + 1) * (p + 1) * fine.dim * esz <= RECORD_LIMIT_BYTES
-    iterates = [BlockVector(eng.lam_a.clone(), check_finite=False)]
+    lean = isinstance(eng, LeanSyncEngine)
+    if lean and record_iterates and (cap + 1) * (p + 1) * fine.dim * esz > RECORD_LIMIT_BYTES:
+        record_iterates = False
+    # the lean engine exists for states that fill HBM: no initial snapshot
+    iterates = [] if (lean and not record_iterates) else [BlockVector(eng.lam_a.clone(), check_finite=False)]
     deltas: list[float] = []
     slice_deltas: list = []
     stop_reason = STOP_KMAX
@@ -539,7 +636,7 @@ def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = N
     while k < cap:
         k += 1
         nxt = eng.lam_b if eng.prev is eng.lam_a else eng.lam_a
-        if record_iterates:
+        if record_iterates and nxt is not eng.prev:
             nxt.copy_(eng.prev)
         # sweep k+1's first F starts while this sweep's chain and the host's
         # delta read finish (discarded if this sweep stops the iteration)
@@ -558,7 +655,8 @@ def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = N
         if k == cap:
             stop_reason = STOP_KMAX
             break
-    final = BlockVector(eng.prev.clone(), check_finite=False)
+    # the engine is not reused: hand its iterate over (lean) or copy it out
+    final = BlockVector(eng.prev if lean else eng.prev.clone(), check_finite=False)
     if not record_iterates:
         iterates.append(final)
     return SyncTrace(iterates=iterates, k_final=k, stop_reason=stop_reason, deltas=deltas, final=final,

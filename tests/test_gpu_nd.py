@@ -202,3 +202,35 @@ def test_fe2d_variants_are_bitwise_identical(gpu, monkeypatch, dtype, shape, ste
     ref = H.ExplicitND(shape, h, 0.2 * h * h, steps).apply(x[1].cpu().numpy())
     tol = 1e-5 if dtype == "float32" else 1e-12
     assert np.max(np.abs(outs[0][1].double().cpu().numpy() - ref)) <= tol * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("shape,p,chunk", [((40, 40), 9, 4), ((16, 16, 16), 7, 3), ((33, 33), 5, 1)])
+def test_lean_engine_is_bitwise_the_standard_engine(gpu, shape, p, chunk):
+    """The in-place engine (2 state copies, for states that fill HBM) gives
+    the same iterates, deltas, k and stop reason as the standard engine."""
+    from paper_2110_10762_b200 import inputs
+    from paper_2110_10762_b200.parareal import LeanSyncEngine
+    import paper_2110_10762_b200.parareal as par
+    n = shape[0]
+    h = 1.0 / (n + 1)
+    span = 20 * 0.15 * h * h
+    u0 = inputs.sine_u0(shape, seed=2)
+    mk = gpu.heat2d_system if len(shape) == 2 else gpu.heat3d_system
+    ivp = mk(n, t_final=p * span, u0=u0)
+    fine = gpu.forward_euler_propagator(ivp, span, 20)
+    coarse = gpu.backward_euler_propagator(ivp, span, 1)
+    std = gpu.run_parareal(coarse, fine, u0, p, 0.0, record_iterates=True)
+    orig = par.LeanSyncEngine.__init__
+
+    def init(self, c, f, pp, chunk_=chunk):
+        orig(self, c, f, pp, chunk=chunk_)
+    par.LeanSyncEngine.__init__ = init
+    try:
+        lean = gpu.run_parareal(coarse, fine, u0, p, 0.0, record_iterates=True, engine="lean")
+    finally:
+        par.LeanSyncEngine.__init__ = orig
+    assert lean.k_final == std.k_final == p and lean.stop_reason == std.stop_reason
+    assert lean.deltas == std.deltas
+    for a, b in zip(lean.iterates, std.iterates):
+        assert np.array_equal(a.data, b.data)
+    assert np.array_equal(lean.final.data, gpu.sequential_fine_solve(fine, u0, p).data)
