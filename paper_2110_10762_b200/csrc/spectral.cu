@@ -21,10 +21,17 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
 #include "pint_internal.cuh"
+
+bool tc_xform_supported(int n);
+void tc_xform_last(const float *src, float *dst, const float *qh0, const float *qh1, int n, int64_t rows,
+                   cudaStream_t s);
+void tc_xform_mid(const float *src, float *dst, const float *qt0, const float *qt1, int n, int planes,
+                  cudaStream_t s);
 
 namespace {
 
@@ -290,7 +297,20 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   // host layout of spec_q: Qh[0] (kh x n0), Qh[1] (kh x n1), QhT[0] (n0 x kh), QhT[1] (n1 x kh)
   const T *qh0 = Q, *qh1 = qh0 + (size_t)kh * n0, *qt0 = qh1 + (size_t)kh * n1, *qt1 = qt0 + (size_t)n0 * kh;
   const double c = op->dt / (op->desc.h * op->desc.h);
+  // fp32 on the tensor cores (3xTF32, tc_xform.cu) where the shape allows;
+  // PINT_TC_XFORM=0 keeps the SIMT GEMMs (measurement)
+  bool tc = false;
+  if constexpr (sizeof(T) == 4) {
+    const char *e = getenv("PINT_TC_XFORM");
+    tc = tc_xform_supported(n) && !(e && atoi(e) == 0);
+  }
   auto xform_last = [&](const T *src, T *dst, int rows) {  // dst = src Q (rows x n)
+    if constexpr (sizeof(T) == 4) {
+      if (tc) {
+        tc_xform_last(src, dst, qh0, qh1, n, rows, s);
+        return;
+      }
+    }
     GemmArgs<T> g{};
     g.A = src;
     g.C = dst;
@@ -309,6 +329,12 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
     gemm<T, 1>(g, 1, s);
   };
   auto xform_mid = [&](const T *src, T *dst) {  // dst_z = Q src_z for every z plane
+    if constexpr (sizeof(T) == 4) {
+      if (tc) {
+        tc_xform_mid(src, dst, qt0, qt1, n, n, s);
+        return;
+      }
+    }
     GemmArgs<T> g{};
     g.B = src;
     g.C = dst;

@@ -74,6 +74,7 @@ def run(name, cfg, tol):
     ms_cg = timed(lambda: cg.apply_ptr(g_in.data_ptr(), g_out.data_ptr(), 1, dim), reps=2)
     out.update({"coarse_solve_ms": ms_g, "coarse_over_fine_slice": ms_g / (ms_f / p), "cg_solve_ms": ms_cg})
     if tol and not cfg.get("fine_only"):
+        pb.run_parareal(coarse, fine, u0, p, cfg["eps"], k_max=1, record_iterates=False)  # warm-up (allocations)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tr = pb.run_parareal(coarse, fine, u0, p, cfg["eps"], record_iterates=False)
