@@ -97,6 +97,7 @@ struct pint_op {
   int64_t cg_nblocks = 0;
   int64_t cg_last_iters = 0;
   void *spec_q = nullptr;      // direct solve: n x n sine transform (T)
+  void *spec_tcq = nullptr;    // direct solve, fp32 tensor-core path: pre-split tf32 tiles of Q
   void *spec_ip = nullptr;     // direct solve: reciprocal pivots [J][mode] (T)
   int spec_J = 0;
 };

@@ -13,11 +13,14 @@
 //   3-D [z][y][x]: W = B Q ;  W_z = Q W_z ;  tridiag_z(1 + 2c + c (mu_kx + mu_ky), -c) ;
 //                  W_z = Q W_z ;  X = W Q
 // with c = dT / h^2. The transforms are dense GEMMs, halved by the parity
-// symmetry of Q (n FLOP per point per transformed axis, FP64/FP32 SIMT tiles; the
-// tensor cores have no FP64 mode worth using on sm_100 and TF32 would not
-// hold the fp32 tolerance), the tridiagonal sweeps are one thread per mode
-// (coalesced across modes). Exact to rounding: no iteration, no tolerance,
-// a pure function of the input bits, stream ordered with no host sync.
+// symmetry of Q (n FLOP per point per transformed axis). fp32 with n a
+// multiple of 256 runs them on the tensor cores in 3xTF32 split precision
+// (tc_xform.cu: tcgen05.mma, TMEM accumulators, the constant Q pre-split on
+// the host); fp64 and other shapes use register-tiled SIMT tiles below (no
+// FP64 tensor-core mode worth using on sm_100). The tridiagonal sweeps are one
+// thread per mode (coalesced across modes). Exact to rounding: no iteration,
+// no tolerance, a pure function of the input bits, stream ordered with no
+// host sync.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,10 +31,9 @@
 #include "pint_internal.cuh"
 
 bool tc_xform_supported(int n);
-void tc_xform_last(const float *src, float *dst, const float *qh0, const float *qh1, int n, int64_t rows,
-                   cudaStream_t s);
-void tc_xform_mid(const float *src, float *dst, const float *qt0, const float *qt1, int n, int planes,
-                  cudaStream_t s);
+std::vector<uint32_t> tc_split_q(int n, const long double *q);
+void tc_xform_last(const float *src, float *dst, const uint32_t *qs, int n, int64_t rows, cudaStream_t s);
+void tc_xform_mid(const float *src, float *dst, const uint32_t *qs, int n, int planes, cudaStream_t s);
 
 namespace {
 
@@ -302,12 +304,12 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   bool tc = false;
   if constexpr (sizeof(T) == 4) {
     const char *e = getenv("PINT_TC_XFORM");
-    tc = tc_xform_supported(n) && !(e && atoi(e) == 0);
+    tc = op->spec_tcq != nullptr && !(e && atoi(e) == 0);
   }
   auto xform_last = [&](const T *src, T *dst, int rows) {  // dst = src Q (rows x n)
     if constexpr (sizeof(T) == 4) {
       if (tc) {
-        tc_xform_last(src, dst, qh0, qh1, n, rows, s);
+        tc_xform_last(src, dst, reinterpret_cast<const uint32_t *>(op->spec_tcq), n, rows, s);
         return;
       }
     }
@@ -331,7 +333,7 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   auto xform_mid = [&](const T *src, T *dst) {  // dst_z = Q src_z for every z plane
     if constexpr (sizeof(T) == 4) {
       if (tc) {
-        tc_xform_mid(src, dst, qt0, qt1, n, n, s);
+        tc_xform_mid(src, dst, reinterpret_cast<const uint32_t *>(op->spec_tcq), n, n, s);
         return;
       }
     }
@@ -450,6 +452,11 @@ void spectral_setup(pint_op *op) {
   PINT_CUDA(cudaMalloc(&op->spec_ip, esz * ipd.size()));
   PINT_CUDA(cudaMemcpy(op->spec_ip, esz == 8 ? (const void *)ipd.data() : (const void *)ipf.data(),
                        esz * ipd.size(), cudaMemcpyHostToDevice));
+  if (esz == 4 && tc_xform_supported((int)n)) {
+    const std::vector<uint32_t> tcq = tc_split_q((int)n, q.data());
+    PINT_CUDA(cudaMalloc(&op->spec_tcq, 4 * tcq.size()));
+    PINT_CUDA(cudaMemcpy(op->spec_tcq, tcq.data(), 4 * tcq.size(), cudaMemcpyHostToDevice));
+  }
   PINT_CUDA(cudaMalloc(&op->spec_q, esz * qd.size()));
   PINT_CUDA(cudaMemcpy(op->spec_q, esz == 8 ? (const void *)qd.data() : (const void *)qf.data(), esz * qd.size(),
                        cudaMemcpyHostToDevice));
@@ -468,6 +475,8 @@ void spectral_apply_batch(pint_op *op, const void *in, void *out, int64_t nbatch
 void spectral_destroy(pint_op *op) {
   if (op->spec_q) cudaFree(op->spec_q);
   if (op->spec_ip) cudaFree(op->spec_ip);
+  if (op->spec_tcq) cudaFree(op->spec_tcq);
+  op->spec_tcq = nullptr;
   op->spec_q = nullptr;
   op->spec_ip = nullptr;
 }

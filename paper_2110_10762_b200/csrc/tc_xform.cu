@@ -29,19 +29,21 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "pint_internal.cuh"
 
 namespace {
 
-constexpr int TM = 128;           // output rows per tile (TMEM lanes, UMMA M)
-constexpr int TN = 128;           // output columns per parity (UMMA N)
-constexpr int BK = 16;            // K per stage (two UMMA K-steps of 8 tf32)
-constexpr int KC = BK / 4;        // 16-byte K chunks per stage
-constexpr int OPB = KC * TM * 16; // bytes of one operand tile (128 rows x 16 K) = 8 KB
-// stage layout: [A0h A0l A1h A1l B0h B0l B1h B1l], 8 operand tiles = 64 KB
-constexpr int STAGE = 8 * OPB;
-constexpr int SMEM = 2 * STAGE + 64;  // + mbarriers and the TMEM base
+constexpr int TM = 128;            // tile rows (TMEM lanes, UMMA M)
+constexpr int TN = 128;            // tile columns per parity (UMMA N)
+constexpr int BK = 8;              // K per stage = one UMMA K-step of tf32
+constexpr int TILE = 2 * TM * 16;  // one operand tile: 2 K chunks x 128 rows x 16 B = 4 KB
+// stage: [data: X0h X0l X1h X1l][constant Q: Q0h Q0l Q1h Q1l], 32 KB
+constexpr int STAGE = 8 * TILE;
+constexpr int QBLK = 4 * TILE;     // constant tiles of one K block (one bulk copy)
+constexpr int SMEM = 2 * STAGE + 64;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -56,21 +58,21 @@ __device__ __forceinline__ void split_tf32(float a, uint32_t &hi, uint32_t &lo) 
   lo = l;
 }
 
-// four consecutive K values of one row -> hi / lo 16-byte chunks of an operand tile
-__device__ __forceinline__ void put4(uint8_t *tile_hi, uint8_t *tile_lo, int kc, int row, const float (&v)[4]) {
+// four consecutive K values of one row -> hi / lo 16-byte chunks of two tiles
+__device__ __forceinline__ void put4(uint32_t tile_hi, uint32_t tile_lo, int kc, int row, const float *v) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) split_tf32(v[i], h[i], l[i]);
   const uint32_t off = (uint32_t)kc * (TM * 16) + (uint32_t)row * 16;
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_addr(tile_hi + off)), "r"(h[0]), "r"(h[1]),
-               "r"(h[2]), "r"(h[3]) : "memory");
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_addr(tile_lo + off)), "r"(l[0]), "r"(l[1]),
-               "r"(l[2]), "r"(l[3]) : "memory");
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tile_hi + off), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+               "r"(h[3]) : "memory");
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tile_lo + off), "r"(l[0]), "r"(l[1]), "r"(l[2]),
+               "r"(l[3]) : "memory");
 }
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-  // SWIZZLE_NONE, K-major: LBO = distance between the two 16-byte K chunks of
-  // an MMA (2048 B), SBO = distance between 8-row core-matrix groups (128 B),
+  // SWIZZLE_NONE, K-major: LBO = distance between the two 16-byte K chunks
+  // (2048 B), SBO = distance between 8-row core-matrix groups (128 B),
   // descriptor version 1 (sm_100)
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -81,7 +83,8 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
 }
 
 // kind::tf32, D fp32, A/B tf32 K-major, M = 128, N = 128
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+constexpr uint32_t IDESC =
+    (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
   asm volatile(
@@ -105,37 +108,38 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 struct TcArgs {
-  const float *src;   // A (FOLD 1) or B (FOLD 2) of the transform
-  const float *h0;    // Qh[0] (FOLD 1: kh x n/2) or QhT[0] (FOLD 2: n/2 x kh)
-  const float *h1;
+  const float *src;     // the data operand: A (FOLD 1) or the z planes of B (FOLD 2)
+  const uint32_t *qs;   // constant operand, pre-split tf32 tiles [qblock][kblock][p][hi|lo][kc][row][4]
   float *dst;
-  int n;              // transform length (even)
-  int kh;             // folded K = n / 2
-  int rows;           // FOLD 1: source rows (M); FOLD 2: columns per plane (= n)
-  int64_t plane;      // FOLD 2: elements per z plane (n * n)
+  int n;                // transform length
+  int kh;               // folded K = n / 2
+  int rows;             // FOLD 1: source rows (M); FOLD 2: columns per plane (= n)
+  int64_t plane;        // FOLD 2: elements per z plane (n * n)
 };
 
 template <int FOLD>
-__global__ void __launch_bounds__(128, 1) xform_tc(const TcArgs g) {
+__global__ void __launch_bounds__(128, 2) xform_tc(const TcArgs g) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + 2 * STAGE);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + 2 * STAGE);  // full[2], empty[2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + 2 * STAGE + 32);
-  const int n = g.n, kh = g.kh, half = n / 2;
-  // tile coordinates
-  const int m0 = blockIdx.x * TM;   // FOLD 1: source rows; FOLD 2: q (output row pairs)
-  const int c0 = blockIdx.y * TN;   // FOLD 1: q (output column pairs); FOLD 2: x
-  const int z = blockIdx.z;         // FOLD 2: plane
-  const float *src = g.src + (FOLD == 2 ? (int64_t)z * g.plane : 0);
-  float *dst = g.dst + (FOLD == 2 ? (int64_t)z * g.plane : 0);
+  const int n = g.n, kh = g.kh, half = n / 2, nkb = kh / BK;
+  const int m0 = blockIdx.x * TM;   // FOLD 1: source rows;  FOLD 2: q (output row pairs)
+  const int c0 = blockIdx.y * TN;   // FOLD 1: q (output column pairs);  FOLD 2: x
+  const float *src = g.src + (FOLD == 2 ? (int64_t)blockIdx.z * g.plane : 0);
+  float *dst = g.dst + (FOLD == 2 ? (int64_t)blockIdx.z * g.plane : 0);
+  // the constant operand's tile rows are the output pairs q of this CTA
+  const uint8_t *qblk = reinterpret_cast<const uint8_t *>(g.qs) +
+                        (size_t)((FOLD == 1 ? c0 : m0) / TM) * nkb * QBLK;
+  const uint32_t s_base = smem_addr(sm);
+  const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[2]);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_addr(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init1(smem_addr(&bars[0]));
-    mbar_init1(smem_addr(&bars[1]));
+    for (int i = 0; i < 4; ++i) mbar_init1(smem_addr(&bars[i]));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -143,109 +147,89 @@ __global__ void __launch_bounds__(128, 1) xform_tc(const TcArgs g) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(tmem_slot);
 
-  const int nk = kh / BK;
-  for (int t = 0; t < nk; ++t) {
-    const int s = t & 1;
-    const int k0 = t * BK;
-    // ---- global loads of K block t (thread = one operand row)
-    float a0[BK], a1[BK], b0[BK], b1[BK];
-    if (FOLD == 1) {
+  // data operand of one K block: d0 (parity 0, "+" fold), d1 (parity 1, "-")
+  float d0[BK], d1[BK];
+  auto load = [&](int kb) {
+    const int k0 = kb * BK;
+    if (FOLD == 1) {  // thread = source row m: A[m][k] +- A[m][n-1-k]
       const int m = m0 + tid;
       if (m < g.rows) {
         const float *row = src + (int64_t)m * n;
 #pragma unroll
         for (int i = 0; i < BK; i += 4) {
-          const float4 f = *reinterpret_cast<const float4 *>(row + k0 + i);
-          const float4 r = *reinterpret_cast<const float4 *>(row + n - 4 - k0 - i);  // A[n-1-k] for k = k0+i..+3
+          const float4 f = __ldcs(reinterpret_cast<const float4 *>(row + k0 + i));
+          const float4 r = __ldcs(reinterpret_cast<const float4 *>(row + n - 4 - k0 - i));
           const float fv[4] = {f.x, f.y, f.z, f.w}, rv[4] = {r.w, r.z, r.y, r.x};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            a0[i + j] = fv[j] + rv[j];
-            a1[i + j] = fv[j] - rv[j];
+            d0[i + j] = fv[j] + rv[j];
+            d1[i + j] = fv[j] - rv[j];
           }
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < BK; ++i) a0[i] = a1[i] = 0.0f;
+        for (int i = 0; i < BK; ++i) d0[i] = d1[i] = 0.0f;
       }
-      // B_p[k][q]: thread = output column pair q (row of the K-major B tile)
-      const int q = c0 + tid;
-#pragma unroll
-      for (int i = 0; i < BK; ++i) {
-        b0[i] = q < half ? __ldg(g.h0 + (int64_t)(k0 + i) * half + q) : 0.0f;
-        b1[i] = q < half ? __ldg(g.h1 + (int64_t)(k0 + i) * half + q) : 0.0f;
-      }
-    } else {
-      // A_p[q][k] = QhT[p][q][k]: thread = output row pair q
-      const int q = m0 + tid;
-      if (q < half) {
-#pragma unroll
-        for (int i = 0; i < BK; i += 4) {
-          const float4 u = *reinterpret_cast<const float4 *>(g.h0 + (int64_t)q * kh + k0 + i);
-          const float4 v = *reinterpret_cast<const float4 *>(g.h1 + (int64_t)q * kh + k0 + i);
-          a0[i] = u.x; a0[i + 1] = u.y; a0[i + 2] = u.z; a0[i + 3] = u.w;
-          a1[i] = v.x; a1[i + 1] = v.y; a1[i + 2] = v.z; a1[i + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < BK; ++i) a0[i] = a1[i] = 0.0f;
-      }
-      // B'_p[k][x] = B[k][x] +- B[n-1-k][x]: thread = column x
+    } else {  // thread = column x: B[k][x] +- B[n-1-k][x]
       const int x = c0 + tid;
 #pragma unroll
       for (int i = 0; i < BK; ++i) {
         float f = 0.0f, r = 0.0f;
         if (x < g.rows) {
-          f = src[(int64_t)(k0 + i) * n + x];
-          r = src[(int64_t)(n - 1 - k0 - i) * n + x];
+          f = __ldcs(src + (int64_t)(k0 + i) * n + x);
+          r = __ldcs(src + (int64_t)(n - 1 - k0 - i) * n + x);
         }
-        b0[i] = f + r;
-        b1[i] = f - r;
+        d0[i] = f + r;
+        d1[i] = f - r;
       }
     }
-    // ---- the stage is free once the MMAs of block t-2 have completed
-    if (t >= 2) mbar_wait(smem_addr(&bars[s]), (uint32_t)(((t - 2) >> 1) & 1));
-    uint8_t *st = sm + s * STAGE;
-#pragma unroll
-    for (int kc = 0; kc < KC; ++kc) {
-      const float va0[4] = {a0[4 * kc], a0[4 * kc + 1], a0[4 * kc + 2], a0[4 * kc + 3]};
-      const float va1[4] = {a1[4 * kc], a1[4 * kc + 1], a1[4 * kc + 2], a1[4 * kc + 3]};
-      const float vb0[4] = {b0[4 * kc], b0[4 * kc + 1], b0[4 * kc + 2], b0[4 * kc + 3]};
-      const float vb1[4] = {b1[4 * kc], b1[4 * kc + 1], b1[4 * kc + 2], b1[4 * kc + 3]};
-      put4(st + 0 * OPB, st + 1 * OPB, kc, tid, va0);
-      put4(st + 2 * OPB, st + 3 * OPB, kc, tid, va1);
-      put4(st + 4 * OPB, st + 5 * OPB, kc, tid, vb0);
-      put4(st + 6 * OPB, st + 7 * OPB, kc, tid, vb1);
+  };
+
+  load(0);
+  for (int t = 0; t < nkb; ++t) {
+    const int s = t & 1;
+    const uint32_t st = s_base + (uint32_t)(s * STAGE);
+    if (t >= 2) mbar_wait(empty0 + 8u * s, (uint32_t)(((t - 2) >> 1) & 1));
+    if (tid == 0) {  // constant tiles of this K block: one bulk copy (TMA engine)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8u * s), "r"(QBLK)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              st + 4u * TILE),
+          "l"(qblk + (size_t)t * QBLK), "r"(QBLK), "r"(full0 + 8u * s)
+          : "memory");
     }
-    // generic-proxy smem writes -> visible to the tensor core (async proxy)
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) {
+      put4(st + 0u * TILE, st + 1u * TILE, kc, tid, d0 + 4 * kc);
+      put4(st + 2u * TILE, st + 3u * TILE, kc, tid, d1 + 4 * kc);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    if (t + 1 < nkb) load(t + 1);  // overlaps the MMAs of block t
     if (tid == 0) {
+      mbar_wait(full0 + 8u * s, (uint32_t)((t >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t base = smem_addr(st);
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t koff = (uint32_t)(2 * ks) * (TM * 16);
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const uint32_t d = tmem + (uint32_t)(p * TN);
-          const uint64_t ah = make_desc(base + (uint32_t)((2 * p) * OPB) + koff);
-          const uint64_t al = make_desc(base + (uint32_t)((2 * p + 1) * OPB) + koff);
-          const uint64_t bh = make_desc(base + (uint32_t)((4 + 2 * p) * OPB) + koff);
-          const uint64_t bl = make_desc(base + (uint32_t)((5 + 2 * p) * OPB) + koff);
-          const uint32_t acc0 = (t > 0 || ks > 0) ? 1u : 0u;
-          mma_tf32(d, al, bh, acc0);  // small terms first
-          mma_tf32(d, ah, bl, 1u);
-          mma_tf32(d, ah, bh, 1u);
-        }
+      for (int p = 0; p < 2; ++p) {
+        const uint32_t d = tmem + (uint32_t)(p * TN);
+        const uint32_t xh = st + (uint32_t)(2 * p) * TILE, xl = xh + TILE;          // data tiles
+        const uint32_t qh = st + (uint32_t)(4 + 2 * p) * TILE, ql = qh + TILE;      // constant tiles
+        // FOLD 1: A = data (rows m), B = Q (rows q); FOLD 2: A = Q (rows q), B = data (rows x)
+        const uint64_t ah = make_desc(FOLD == 1 ? xh : qh), al = make_desc(FOLD == 1 ? xl : ql);
+        const uint64_t bh = make_desc(FOLD == 1 ? qh : xh), bl = make_desc(FOLD == 1 ? ql : xl);
+        const uint32_t acc0 = t > 0 ? 1u : 0u;
+        mma_tf32(d, al, bh, acc0);  // small terms first
+        mma_tf32(d, ah, bl, 1u);
+        mma_tf32(d, ah, bh, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_addr(&bars[s]))
+                       empty0 + 8u * s)
                    : "memory");
     }
   }
-  // ---- all MMAs issued by thread 0 complete with the last commit
-  mbar_wait(smem_addr(&bars[(nk - 1) & 1]), (uint32_t)(((nk - 1) >> 1) & 1));
+  // all MMAs of thread 0 complete with its last commit
+  mbar_wait(empty0 + 8u * ((nkb - 1) & 1), (uint32_t)(((nkb - 1) >> 1) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- epilogue: warp w owns TMEM lanes (tile rows) 32w .. 32w+31
@@ -276,8 +260,8 @@ __global__ void __launch_bounds__(128, 1) xform_tc(const TcArgs g) {
         float4 *out = reinterpret_cast<float4 *>(dst + (int64_t)m * n + 2 * (c0 + cc));
 #pragma unroll
         for (int j = 0; j < 32; j += 2)
-          out[j / 2] = make_float4(__uint_as_float(v[0][j]), __uint_as_float(v[1][j]), __uint_as_float(v[0][j + 1]),
-                                   __uint_as_float(v[1][j + 1]));
+          __stcs(out + j / 2, make_float4(__uint_as_float(v[0][j]), __uint_as_float(v[1][j]),
+                                          __uint_as_float(v[0][j + 1]), __uint_as_float(v[1][j + 1])));
       }
     } else {
       // rows 2q + p, columns x = c0 + cc .. +31
@@ -288,8 +272,8 @@ __global__ void __launch_bounds__(128, 1) xform_tc(const TcArgs g) {
           float4 *out = reinterpret_cast<float4 *>(dst + (int64_t)(2 * q + p) * n + c0 + cc);
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
-            out[j / 4] = make_float4(__uint_as_float(v[p][j]), __uint_as_float(v[p][j + 1]),
-                                     __uint_as_float(v[p][j + 2]), __uint_as_float(v[p][j + 3]));
+            __stcs(out + j / 4, make_float4(__uint_as_float(v[p][j]), __uint_as_float(v[p][j + 1]),
+                                            __uint_as_float(v[p][j + 2]), __uint_as_float(v[p][j + 3])));
         }
       }
     }
@@ -301,26 +285,56 @@ __global__ void __launch_bounds__(128, 1) xform_tc(const TcArgs g) {
 
 }  // namespace
 
-// Eligible shapes: n a multiple of 64 (kh = n/2 a multiple of the 16-deep K
-// stage, output pairs in whole 32-column epilogue chunks).
-bool tc_xform_supported(int n) { return n >= 64 && n % 64 == 0; }
+// Eligible shapes: n a multiple of 256 (output pairs in whole 128-row
+// tiles, kh = n/2 a multiple of the K block).
+bool tc_xform_supported(int n) { return n >= 256 && n % 256 == 0; }
 
-// dst = src Q along the fastest axis (rows x n, row-major), Q the folded sine transform
-void tc_xform_last(const float *src, float *dst, const float *qh0, const float *qh1, int n, int64_t rows,
-                   cudaStream_t s) {
-  TcArgs g{src, qh0, qh1, dst, n, n / 2, (int)rows, 0};
+// The constant operand, split once on the host from the long-double sine
+// transform (better than splitting its fp32 rounding): tiles
+// [q block][k block][parity][hi|lo][kc][row q][4 k], tf32 bit patterns.
+// Qh[p][k][q] = Q[k][2q + p] (FOLD 1 B, rows q) equals QhT[p][q][k] (FOLD 2 A).
+static uint32_t tf32_rna(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return u;
+  return (u + 0x1000u) & 0xffffe000u;
+}
+std::vector<uint32_t> tc_split_q(int n, const long double *q) {
+  const int half = n / 2, kh = n / 2, nqb = half / TM, nkb = kh / BK;
+  std::vector<uint32_t> out((size_t)nqb * nkb * QBLK / 4);
+  for (int qb = 0; qb < nqb; ++qb)
+    for (int kb = 0; kb < nkb; ++kb)
+      for (int p = 0; p < 2; ++p)
+        for (int hl = 0; hl < 2; ++hl)
+          for (int kc = 0; kc < 2; ++kc)
+            for (int r = 0; r < TM; ++r)
+              for (int e = 0; e < 4; ++e) {
+                const int k = kb * BK + kc * 4 + e, qq = qb * TM + r;
+                const long double v = q[(size_t)k * n + 2 * qq + p];
+                const uint32_t hbits = tf32_rna((float)v);
+                float hf;
+                memcpy(&hf, &hbits, 4);
+                const uint32_t bits = hl == 0 ? hbits : tf32_rna((float)(v - (long double)hf));
+                const size_t idx = ((((((size_t)qb * nkb + kb) * 2 + p) * 2 + hl) * 2 + kc) * TM + r) * 4 + e;
+                out[idx] = bits;
+              }
+  return out;
+}
+
+// dst = src Q along the fastest axis (rows x n, row-major)
+void tc_xform_last(const float *src, float *dst, const uint32_t *qs, int n, int64_t rows, cudaStream_t s) {
+  TcArgs g{src, qs, dst, n, n / 2, (int)rows, 0};
   PINT_CUDA(cudaFuncSetAttribute(xform_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  dim3 grid((unsigned)((rows + TM - 1) / TM), (unsigned)((n / 2 + TN - 1) / TN), 1);
+  dim3 grid((unsigned)((rows + TM - 1) / TM), (unsigned)(n / 2 / TN), 1);
   xform_tc<1><<<grid, 128, SMEM, s>>>(g);
   PINT_CUDA(cudaGetLastError());
 }
 
 // dst_z = Q src_z for each of the `planes` n x n planes
-void tc_xform_mid(const float *src, float *dst, const float *qt0, const float *qt1, int n, int planes,
-                  cudaStream_t s) {
-  TcArgs g{src, qt0, qt1, dst, n, n / 2, n, (int64_t)n * n};
+void tc_xform_mid(const float *src, float *dst, const uint32_t *qs, int n, int planes, cudaStream_t s) {
+  TcArgs g{src, qs, dst, n, n / 2, n, (int64_t)n * n};
   PINT_CUDA(cudaFuncSetAttribute(xform_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  dim3 grid((unsigned)((n / 2 + TM - 1) / TM), (unsigned)((n + TN - 1) / TN), (unsigned)planes);
+  dim3 grid((unsigned)(n / 2 / TM), (unsigned)(n / TN), (unsigned)planes);
   xform_tc<2><<<grid, 128, SMEM, s>>>(g);
   PINT_CUDA(cudaGetLastError());
 }
