@@ -304,7 +304,9 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   bool tc = false;
   if constexpr (sizeof(T) == 4) {
     const char *e = getenv("PINT_TC_XFORM");
-    tc = op->spec_tcq != nullptr && !(e && atoi(e) == 0);
+    // 3-D only: a 2-D transform (n rows) is too small a grid for the tensor-core tiles
+    // (1024^2: 0.376 vs 0.349 ms SIMT, scripts/tc_xform_probe.py)
+    tc = op->spec_tcq != nullptr && op->desc.ndim == 3 && !(e && atoi(e) == 0);
   }
   auto xform_last = [&](const T *src, T *dst, int rows) {  // dst = src Q (rows x n)
     if constexpr (sizeof(T) == 4) {
@@ -452,7 +454,7 @@ void spectral_setup(pint_op *op) {
   PINT_CUDA(cudaMalloc(&op->spec_ip, esz * ipd.size()));
   PINT_CUDA(cudaMemcpy(op->spec_ip, esz == 8 ? (const void *)ipd.data() : (const void *)ipf.data(),
                        esz * ipd.size(), cudaMemcpyHostToDevice));
-  if (esz == 4 && tc_xform_supported((int)n)) {
+  if (esz == 4 && op->desc.ndim == 3 && tc_xform_supported((int)n)) {
     const std::vector<uint32_t> tcq = tc_split_q((int)n, q.data());
     PINT_CUDA(cudaMalloc(&op->spec_tcq, 4 * tcq.size()));
     PINT_CUDA(cudaMemcpy(op->spec_tcq, tcq.data(), 4 * tcq.size(), cudaMemcpyHostToDevice));
