@@ -213,6 +213,85 @@ void gemm(const GemmArgs<T> &g, int batch, cudaStream_t s) {
   PINT_CUDA(cudaGetLastError());
 }
 
+// Few transverse modes (2-D grids: n systems of length n) leave the
+// one-thread-per-mode sweep on a handful of SMs (C3: 1024 threads = 8 SMs,
+// 169 us). Here each system is split into MC chunks: warp-of-chunks x
+// system-lane threads (lanes = consecutive systems, so every row access is
+// coalesced), each thread composes its chunk's affine map of the first-order
+// recurrences (forward g_j = (c g_{j-1} + d_j) p_j^-1; backward
+// x_j = g_j + c p_j^-1 x_{j+1}), the chunk entry values are chained through
+// shared memory, and every chunk is recomputed from its exact entry value
+// with the sequential formula. Same operator, rounding-level differences
+// only (the recurrences contract: c p_j^-1 < 1).
+template <typename T, int MC, int SYS>
+__global__ void __launch_bounds__(MC * SYS)
+modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_t nsys, double c,
+                      int64_t steps) {
+  __shared__ double cmp[2][MC][SYS];  // chunk maps (A, B)
+  __shared__ double entry[MC + 1][SYS];
+  const int w = threadIdx.x / SYS, sl = threadIdx.x % SYS;
+  const int64_t i = (int64_t)blockIdx.x * SYS + sl;
+  const bool live = i < nsys;
+  const int L = (n + MC - 1) / MC, j0 = w * L, j1 = min(n, j0 + L);  // chunk [j0, j1)
+  const double ipinf = live ? (double)ipt[(int64_t)(J - 1) * nsys + i] : 0.0;
+  auto ipat = [&](int j) { return j < J ? (double)ipt[(int64_t)j * nsys + i] : ipinf; };
+  for (int64_t s = 0; s < steps; ++s) {
+    // ---- forward: g_end = A g_in + B over the chunk
+    double A = 1.0, B = 0.0;
+    if (live)
+      for (int j = j0; j < j1; ++j) {
+        const double ip = ipat(j);
+        A = (c * ip) * A;
+        B = fma(c, B, (double)u[(int64_t)j * nsys + i]) * ip;
+      }
+    cmp[0][w][sl] = A;
+    cmp[1][w][sl] = B;
+    __syncthreads();
+    if (w == 0) {
+      double g = 0.0;
+      for (int q = 0; q < MC; ++q) {
+        entry[q][sl] = g;
+        g = fma(cmp[0][q][sl], g, cmp[1][q][sl]);
+      }
+    }
+    __syncthreads();
+    double g = entry[w][sl];
+    if (live)
+      for (int j = j0; j < j1; ++j) {
+        g = fma(c, g, (double)u[(int64_t)j * nsys + i]) * ipat(j);
+        u[(int64_t)j * nsys + i] = (T)g;
+      }
+    __syncthreads();
+    // ---- backward: x_j = g_j + e_j x_{j+1}, e_j = c / p_j (e_{n-1} = 0)
+    double C = 1.0, D = 0.0;
+    if (live)
+      for (int j = j1 - 1; j >= j0; --j) {
+        const double e = j == n - 1 ? 0.0 : c * ipat(j);
+        C = e * C;
+        D = fma(e, D, (double)u[(int64_t)j * nsys + i]);
+      }
+    cmp[0][w][sl] = C;
+    cmp[1][w][sl] = D;
+    __syncthreads();
+    if (w == 0) {
+      double x = 0.0;
+      for (int q = MC - 1; q >= 0; --q) {
+        entry[q][sl] = x;
+        x = fma(cmp[0][q][sl], x, cmp[1][q][sl]);
+      }
+    }
+    __syncthreads();
+    double x = entry[w][sl];
+    if (live)
+      for (int j = j1 - 1; j >= j0; --j) {
+        const double e = j == n - 1 ? 0.0 : c * ipat(j);
+        x = fma(e, x, (double)u[(int64_t)j * nsys + i]);
+        u[(int64_t)j * nsys + i] = (T)x;
+      }
+    __syncthreads();
+  }
+}
+
 // One thread per transverse mode: `steps` backward-Euler solves along the
 // slowest axis (n points, `nsys` modes interleaved: point j of mode i at
 // u[j * nsys + i]). The reciprocal pivots 1/p_j (p_0 = d, p_j = d - c^2 /
@@ -361,8 +440,15 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   const unsigned threads = 128;
   if (op->desc.ndim == 2) {
     xform_last(b, w1, n);
-    modal_tridiag<T><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
-        w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
+    const char *mc = getenv("PINT_MODAL_CHUNKED");
+    if (n >= 256 && !(mc && atoi(mc) == 0)) {
+      constexpr int MC = 64, SYS = 16;
+      modal_tridiag_chunked<T, MC, SYS><<<(unsigned)((n + SYS - 1) / SYS), MC * SYS, 0, s>>>(
+          w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
+    } else {
+      modal_tridiag<T><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
+          w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
+    }
     PINT_CUDA(cudaGetLastError());
     xform_last(w1, x, n);
   } else {
