@@ -454,6 +454,7 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   } else {
     xform_last(b, w1, (int)n2);
     xform_mid(w1, w2);
+    // (the chunked sweep measured slower here: 3-D grids have n^2 modes, 0.510 vs 0.480 ms at C4)
     modal_tridiag<T><<<(unsigned)((n2 + threads - 1) / threads), threads, 0, s>>>(
         w2, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n2, c, op->desc.steps);
     PINT_CUDA(cudaGetLastError());
