@@ -43,7 +43,10 @@ constexpr int TILE = 2 * TM * 16;  // one operand tile: 2 K chunks x 128 rows x 
 // stage: [data: X0h X0l X1h X1l][constant Q: Q0h Q0l Q1h Q1l], 32 KB
 constexpr int STAGE = 8 * TILE;
 constexpr int QBLK = 4 * TILE;     // constant tiles of one K block (one bulk copy)
-constexpr int SMEM = 2 * STAGE + 64;
+// 2 * STAGE + barriers is 64 KB; request 100 KB so at most two CTAs share an
+// SM — exactly the TMEM they need (2 x 256 columns), no third CTA blocking in
+// tcgen05.alloc
+constexpr int SMEM = 100 * 1024;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
