@@ -82,3 +82,22 @@ def test_cli_device_runs_and_table(gpu, tmp_path):
     with open(tmp_path / "t.csv", newline="", encoding="utf-8") as fh:
         t = list(csv.DictReader(fh))
     assert list(t[0].keys()) == TABLE_COLUMNS and t[-1]["schedule"] == "device/s2"
+
+
+def test_cli_3d_config_with_stream_async_runs(gpu, tmp_path):
+    """A 3-D configuration through the driver: explicit fine, direct coarse,
+    a device async run on CUDA streams with two slice domains."""
+    from paper_2110_10762_b200.cli import main
+    cfg = {"label": "c4-small", "p": 6, "epsilon": 1e-5, "dtype": "float32", "analysis": False,
+           "problem": {"name": "heat3d", "n": 24, "t_final": 6 * 40 * 0.15 / 25 ** 2, "seed": 0},
+           "fine": {"rule": "forward-euler", "steps": 40}, "coarse": {"rule": "backward-euler", "steps": 1},
+           "device_runs": [{"seed": 3, "domains": 2}]}
+    cfg_path = tmp_path / "c.json"
+    cfg_path.write_text(json.dumps(cfg), encoding="utf-8")
+    out = tmp_path / "out"
+    assert main(["run", "--config", str(cfg_path), "--out", str(out)]) == 0
+    rows = _rows(out)
+    assert [r["mode"] for r in rows] == ["sequential", "sync", "async-device"]
+    assert rows[1]["stop_reason"] in ("threshold", "exact") and float(rows[1]["error_vs_oracle"]) < 1e-4
+    assert rows[2]["stop_reason"] == "converged" and float(rows[2]["error_vs_oracle"]) < 1e-4
+    assert rows[2]["sync_factor"] == ""  # analysis off
