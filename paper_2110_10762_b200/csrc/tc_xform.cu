@@ -43,10 +43,15 @@ constexpr int TILE = 2 * TM * 16;  // one operand tile: 2 K chunks x 128 rows x 
 // stage: [data: X0h X0l X1h X1l][constant Q: Q0h Q0l Q1h Q1l], 32 KB
 constexpr int STAGE = 8 * TILE;
 constexpr int QBLK = 4 * TILE;     // constant tiles of one K block (one bulk copy)
-// 2 * STAGE + barriers is 64 KB; request 100 KB so at most two CTAs share an
-// SM — exactly the TMEM they need (2 x 256 columns), no third CTA blocking in
-// tcgen05.alloc
-constexpr int SMEM = 100 * 1024;
+// raw data ring: each thread streams its own row (FOLD 1) / column (FOLD 2)
+// of RAWS K blocks ahead with cp.async (forward + reversed 8 values = 64 B
+// per thread per block), then folds and splits from shared memory
+constexpr int RAWS = 6;
+constexpr int RAWB = 128 * 64;  // one K block of raw data for the CTA (8 KB)
+constexpr int RAW_OFF = 2 * STAGE + 64;
+// 2 x 32 KB UMMA stages + barriers + 48 KB ring = 112 KB: two CTAs per SM,
+// exactly the TMEM they need (2 x 256 columns)
+constexpr int SMEM = RAW_OFF + RAWS * RAWB;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -150,48 +155,73 @@ __global__ void __launch_bounds__(128, 2) xform_tc(const TcArgs g) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(tmem_slot);
 
-  // data operand of one K block: d0 (parity 0, "+" fold), d1 (parity 1, "-")
-  float d0[BK], d1[BK];
-  auto load = [&](int kb) {
-    const int k0 = kb * BK;
-    if (FOLD == 1) {  // thread = source row m: A[m][k] +- A[m][n-1-k]
-      const int m = m0 + tid;
-      if (m < g.rows) {
-        const float *row = src + (int64_t)m * n;
+  // raw ring: K block slot = 4 chunks of 16 B per thread, chunk-major
+  // ([chunk][thread][16 B]) so the fold's 16-byte reads are conflict-free.
+  // chunks: 0, 1 = values k0..k0+7; 2, 3 = the mirrored values
+  // (FOLD 1: A[m][n-8-k0 .. n-1-k0] in memory order; FOLD 2: B[n-1-k0-i][x], i = 0..7)
+  const uint32_t raw_base = s_base + (uint32_t)RAW_OFF + (uint32_t)tid * 16u;
+  auto issue = [&](int kb) {  // cp.async of K block kb into ring slot kb % RAWS (always commits a group)
+    if (kb < nkb) {
+      const int k0 = kb * BK;
+      const uint32_t dst = raw_base + (uint32_t)((kb % RAWS) * RAWB);
+      if (FOLD == 1) {  // thread = source row m
+        const int m = m0 + tid;
+        if (m < g.rows) {
+          const float *row = src + (int64_t)m * n;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(row + k0) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 2048u), "l"(row + k0 + 4)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 4096u), "l"(row + n - 8 - k0)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 6144u), "l"(row + n - 4 - k0)
+                       : "memory");
+        }
+      } else {  // thread = column x
+        const int x = c0 + tid;
+        if (x < g.rows) {
 #pragma unroll
-        for (int i = 0; i < BK; i += 4) {
-          const float4 f = __ldcs(reinterpret_cast<const float4 *>(row + k0 + i));
-          const float4 r = __ldcs(reinterpret_cast<const float4 *>(row + n - 4 - k0 - i));
-          const float fv[4] = {f.x, f.y, f.z, f.w}, rv[4] = {r.w, r.z, r.y, r.x};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            d0[i + j] = fv[j] + rv[j];
-            d1[i + j] = fv[j] - rv[j];
+          for (int i = 0; i < BK; ++i) {
+            const uint32_t o = (uint32_t)(i / 4) * 2048u + 4u * (uint32_t)(i % 4);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + o),
+                         "l"(src + (int64_t)(k0 + i) * n + x) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4096u + o),
+                         "l"(src + (int64_t)(n - 1 - k0 - i) * n + x) : "memory");
           }
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < BK; ++i) d0[i] = d1[i] = 0.0f;
       }
-    } else {  // thread = column x: B[k][x] +- B[n-1-k][x]
-      const int x = c0 + tid;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // fold K block kb from the ring: d0 = f + r, d1 = f - r
+  float d0[BK], d1[BK];
+  auto fold = [&](int kb) {
+    const uint8_t *rb = sm + RAW_OFF + (kb % RAWS) * RAWB + tid * 16;
+    const bool ok = FOLD == 1 ? (m0 + tid < g.rows) : (c0 + tid < g.rows);
+    float v[16];
 #pragma unroll
-      for (int i = 0; i < BK; ++i) {
-        float f = 0.0f, r = 0.0f;
-        if (x < g.rows) {
-          f = __ldcs(src + (int64_t)(k0 + i) * n + x);
-          r = __ldcs(src + (int64_t)(n - 1 - k0 - i) * n + x);
-        }
-        d0[i] = f + r;
-        d1[i] = f - r;
-      }
+    for (int c = 0; c < 4; ++c) {
+      const float4 q = *reinterpret_cast<const float4 *>(rb + c * 2048);
+      v[4 * c] = q.x;
+      v[4 * c + 1] = q.y;
+      v[4 * c + 2] = q.z;
+      v[4 * c + 3] = q.w;
+    }
+#pragma unroll
+    for (int i = 0; i < BK; ++i) {
+      const float f = ok ? v[i] : 0.0f;
+      const float r = ok ? (FOLD == 1 ? v[8 + (BK - 1 - i)] : v[8 + i]) : 0.0f;
+      d0[i] = f + r;
+      d1[i] = f - r;
     }
   };
 
-  load(0);
+  for (int q = 0; q < RAWS - 1; ++q) issue(q);
   for (int t = 0; t < nkb; ++t) {
     const int s = t & 1;
     const uint32_t st = s_base + (uint32_t)(s * STAGE);
+    issue(t + RAWS - 1);  // keep RAWS - 1 K blocks in flight
+    asm volatile("cp.async.wait_group %0;" ::"n"(RAWS - 1) : "memory");  // block t (this thread's copies) landed
+    fold(t);
     if (t >= 2) mbar_wait(empty0 + 8u * s, (uint32_t)(((t - 2) >> 1) & 1));
     if (tid == 0) {  // constant tiles of this K block: one bulk copy (TMA engine)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8u * s), "r"(QBLK)
@@ -209,7 +239,6 @@ __global__ void __launch_bounds__(128, 2) xform_tc(const TcArgs g) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (t + 1 < nkb) load(t + 1);  // overlaps the MMAs of block t
     if (tid == 0) {
       mbar_wait(full0 + 8u * s, (uint32_t)((t >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
