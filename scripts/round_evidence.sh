@@ -19,4 +19,7 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:fe2d
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:fe3d_tile -c 1 \
   -o gpurun_out/prof_fe3d -f python scripts/profile_nd.py c4_f32 16 3 > gpurun_out/ncu_fe3d.log 2>&1
 timeout 900 python scripts/bench_configs.py all --tol > gpurun_out/nd_configs.jsonl 2>&1
+timeout 300 python scripts/c1_time.py > gpurun_out/c1_time.json 2>&1
+timeout 600 python scripts/c5_lean.py 1e-5 > gpurun_out/c5_lean.json 2>&1
+timeout 900 python scripts/async_nd.py 1e-5 > gpurun_out/async_nd_c4.jsonl 2>&1
 ls -la gpurun_out | head -40
