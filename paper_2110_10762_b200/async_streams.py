@@ -22,7 +22,6 @@ peer-to-peer copy into the next GPU's mailbox).
 """
 from __future__ import annotations
 
-import random
 import time
 
 import numpy as np
@@ -145,7 +144,6 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
         lanes_by_dom[ln.domain].append(ln)
         all_lanes.append(ln)
     tickets = [0] * domains
-    rng = random.Random(seed)
     spin_cycles_per_tf = 0.0
     if delay_frac > 0.0:  # injected delay U(0, delay_frac) * t_F per activation
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -213,7 +211,8 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
                 mb_readers[i][dst_slot] = []
             ln.fine.apply_ptr(remb[i].data_ptr(), ln.f.data_ptr(), 1, n, stream=st.cuda_stream)
             if delay_frac > 0.0:
-                torch.cuda._sleep(int(rng.random() * delay_frac * spin_cycles_per_tf))
+                # U(0, delay_frac) * t_F keyed by (seed, slice, activation), as in the kernel runtime
+                torch.cuda._sleep(int(_unit(seed, i, int(counts[i])) * delay_frac * spin_cycles_per_tf))
             if ev_src is not None:
                 st.wait_event(ev_src)
             ln.fresh[0].copy_(row, non_blocking=True)
@@ -322,6 +321,17 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
     if stop_reason == "max_events":
         raise HorizonExhausted(f"no stop condition met within {max_events} activations", res)
     return res
+
+
+def _unit(seed: int, i: int, count: int) -> float:
+    """splitmix64 of (seed, slice, activation) -> U[0, 1) (async_rt.cu mix64)."""
+    m = (1 << 64) - 1
+    z = (seed ^ ((i << 32) & m) ^ count) & m
+    z = (z + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    z ^= z >> 31
+    return (z >> 11) * (1.0 / 9007199254740992.0)
 
 
 def _ptr(t):
