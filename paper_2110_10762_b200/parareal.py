@@ -396,6 +396,15 @@ class SyncEngine:
         main.wait_stream(dn)
         self.prev = nxt
 
+    def finish(self) -> None:
+        """Join a speculative launch that the run did not use into the current
+        stream: its F results are discarded, but the buffers it writes must
+        not be released (or reused by the caching allocator) before it ends."""
+        spec = getattr(self, "_spec", None)
+        self._spec = None
+        if spec is not None:
+            torch.cuda.current_stream(self.fine.device).wait_event(spec[2])
+
     def _spec_stream(self):
         st = getattr(self, "_spec_st", None)
         if st is None:
@@ -655,6 +664,8 @@ def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = N
         if k == cap:
             stop_reason = STOP_KMAX
             break
+    if hasattr(eng, "finish"):
+        eng.finish()
     # the engine is not reused: hand its iterate over (lean) or copy it out
     final = BlockVector(eng.prev if lean else eng.prev.clone(), check_finite=False)
     if not record_iterates:
