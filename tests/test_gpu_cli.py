@@ -101,3 +101,24 @@ def test_cli_3d_config_with_stream_async_runs(gpu, tmp_path):
     assert rows[1]["stop_reason"] in ("threshold", "exact") and float(rows[1]["error_vs_oracle"]) < 1e-4
     assert rows[2]["stop_reason"] == "converged" and float(rows[2]["error_vs_oracle"]) < 1e-4
     assert rows[2]["sync_factor"] == ""  # analysis off
+
+
+def test_cli_runs_are_byte_deterministic(gpu, tmp_path):
+    """Reference criterion 11 (test_acceptance.py:380-416, test_cli.py:125-131):
+    reruns of a config without device runs or measured costs write
+    byte-identical report.json and summary.csv (and traces)."""
+    from paper_2110_10762_b200.cli import main
+    cfg = RUNS["scalar"]["config"]
+    cfg_path = tmp_path / "c.json"
+    cfg_path.write_text(json.dumps(cfg), encoding="utf-8")
+    outs = []
+    for tag in ("a", "b"):
+        out = tmp_path / tag
+        assert main(["run", "--config", str(cfg_path), "--out", str(out), "--traces"]) == RUNS["scalar"]["exit_code"]
+        outs.append(out)
+    for name in ("report.json", "summary.csv"):
+        assert (outs[0] / name).read_bytes() == (outs[1] / name).read_bytes(), name
+    ta = sorted(p.name for p in (outs[0] / "traces").iterdir())
+    assert ta == sorted(p.name for p in (outs[1] / "traces").iterdir()) and ta
+    for name in ta:
+        assert (outs[0] / "traces" / name).read_bytes() == (outs[1] / "traces" / name).read_bytes(), name
