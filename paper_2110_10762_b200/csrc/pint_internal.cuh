@@ -89,6 +89,7 @@ struct pint_op {
   int sweep_cluster = 1;
   int batch_wave_slices = 0;  // slices of apply_batch resident at once (0 = unknown)
   int batch_minb = 2;  // CTAs per SM the fine kernel is register-budgeted for (1 or 2)
+  bool fused_sweep = true;  // the fused coarse sweep's shared memory fits one CTA
   // n-D
   int64_t nx = 1, ny = 1, nz = 1;
   void *cg_work = nullptr;   // CG scratch

@@ -113,6 +113,12 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
   P.l_last = (int)((N - 1) % CH);
   const int64_t threads_needed = (N + CH - 1) / CH;
   P.nW = (int)((threads_needed + 31) / 32);
+  // Pad with virtual warps (all-zero chunks, masked separators: decoupled
+  // unknowns) so that every cluster split is whole warps: the batch kernel
+  // splits a slice into nW/8 CTAs of 256 threads, the fused sweep into
+  // min(16, nW/4) CTAs (multiples of 32 threads need nW % 16 == 0 above 64).
+  if (P.nW > 8) P.nW = (P.nW + 7) / 8 * 8;
+  if (P.nW > 64) P.nW = (P.nW + 15) / 16 * 16;
   P.T = 32 * P.nW;
   P.J = (P.nW + 31) / 32;
   if (P.J == 3) P.J = 4;
@@ -577,6 +583,17 @@ void tri1d_setup(pint_op *op) {
   // CTA split of the T threads of a slice (does not change the arithmetic)
   op->batch_cluster = std::max(1, pl.T / 256);
   op->sweep_cluster = std::min(16, std::max(1, pl.T / 128));
+  {
+    // fused sweep: factor table + gather buffers + a staging row of 3 CH + 2
+    // doubles per thread (tri1d_sweep_kernel); beyond ~100k points it no
+    // longer fits and the sync engine uses the generic (per-slice) sweep
+    const int TBs = pl.T / op->sweep_cluster;
+    const size_t need = smem_bytes(pl, TBs) + sizeof(double) * (size_t)TBs * (3 * pl.CH + 2);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 232448;
+    op->fused_sweep = need <= (size_t)optin;
+  }
   if (const char *mb = getenv("PINT_TRI_MINB")) op->batch_minb = atoi(mb) == 1 ? 1 : 2;
   if (const char *bc = getenv("PINT_TRI_BATCH_CL")) {
     const int v = atoi(bc);
@@ -613,6 +630,7 @@ void tri1d_coarse_init(pint_op *op, double *lam, int64_t p, double *gcache, cuda
 void tri1d_sweep(pint_op *op, const double *prev, double *next, const double *fv, double *gcache, int64_t k,
                  int64_t p, double *deltas, int32_t *nonfinite, cudaStream_t s, int chain) {
   if (p * op->plan.steps >= (int64_t)1 << 31) pint_throw(PINT_EARG, "p * steps must stay below 2^31");
+  if (!op->fused_sweep) pint_throw(PINT_EUNSUPPORTED, "the fused coarse sweep does not fit this grid (use the generic sweep)");
   run_any(TriKind::Sweep, op, 1, op->sweep_cluster, s, nullptr, nullptr, 0, nullptr, gcache, p, prev, next, fv,
           k, deltas, nonfinite, chain);
 }

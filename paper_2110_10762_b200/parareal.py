@@ -181,7 +181,7 @@ class SyncEngine:
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.fonly = torch.zeros(p + 1, dtype=torch.bool, device=dev)  # generic sweep: per-slice F-only mask
         self.host = torch.zeros(2, dtype=torch.float64).pin_memory() if torch.cuda.is_available() else None
-        self.fused = coarse.is_tridiagonal
+        self.fused = coarse.is_tridiagonal and bool(coarse.info.fused_sweep)
         self.prev = self.lam_a
         self.lib = _native.load_library()
         # pipelining: F runs in wave-sized chunks of slices on the current
