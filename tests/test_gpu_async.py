@@ -115,6 +115,22 @@ def test_device_async_quiescence_is_the_sequential_solution(gpu, delay):
     assert res.kappa >= 1 and res.activations >= p
 
 
+@pytest.mark.parametrize("n,p,domains", [(65537, 24, 1), (100_000, 20, 2)])
+def test_device_async_ragged_large_grid_quiescence(gpu, n, p, domains):
+    """Ragged C2-scale grids (10- and 14-CTA clusters, padded warps, tail
+    chunks): the persistent runtime still quiesces on the sequential fine
+    solution bitwise."""
+    from paper_2110_10762_b200.inputs import sine_u0_1d
+    u0 = sine_u0_1d(n, 16, 5)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1 / p, 10)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    seq = gpu.sequential_fine_solve(fine, u0, p).data
+    res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, delay_frac=0.1, seed=n, domains=domains)
+    assert res.stop_reason == "converged"
+    assert np.array_equal(res.final.data, seq)
+
+
 def test_device_async_epsilon_stop_reaches_sync_solution(gpu):
     from oracle import heat_oracle as H
     n, p = 1024, 16
