@@ -12,6 +12,7 @@ from .async_engine import (
     POLICY_ADVERSARIAL,
     POLICY_RANDOM_FAIR,
     POLICY_ROUND_ROBIN,
+    AsyncMapping,
     AsyncSchedule,
     AsyncTrace,
     EngineView,
@@ -23,7 +24,9 @@ from .async_engine import (
 from .async_parareal import (
     FRESH_SLOT,
     REMEMBERED_SLOT,
+    async_parareal_mapping,
     async_stop_check,
+    simulate_async,
     run_async_parareal,
     simulate_parareal_async,
     run_async_parareal_device,

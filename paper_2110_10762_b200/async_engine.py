@@ -14,8 +14,8 @@ runtime with real staleness is ``async_parareal.run_async_parareal_device``.
 from __future__ import annotations
 
 import json
-from dataclasses import dataclass
-from typing import NamedTuple
+from dataclasses import dataclass, field
+from typing import Callable, NamedTuple
 
 import numpy as np
 
@@ -26,6 +26,44 @@ POLICIES = (POLICY_ROUND_ROBIN, POLICY_RANDOM_FAIR, POLICY_ADVERSARIAL)
 
 STOP_PREDICATE = "stop-predicate"
 STOP_QUIESCENCE = "quiescence"
+
+
+@dataclass
+class AsyncMapping:
+    """Componentwise fixed-point map read from slot-indexed predecessor
+    readings (async_engine.py:83-120): ``read_set[i]`` lists the (source,
+    slot) pairs component i consumes, ``persistent_slots`` maps a slot to the
+    base slot whose previously consumed version it replays. Same validation
+    and exceptions as the reference. ``simulate_async`` runs the Parareal
+    mapping built by ``async_parareal.async_parareal_mapping`` on the GPU."""
+
+    n_updatable: int
+    arity: int
+    eval_fn: Callable
+    read_set: dict
+    persistent_slots: dict = field(default_factory=dict)
+    propagators: tuple | None = None  # (coarse, fine) for the Parareal mapping
+
+    def __post_init__(self):
+        from .errors import DimensionError
+        if self.n_updatable < 1:
+            raise ValueError("need at least one updatable component")
+        for i in range(1, self.n_updatable + 1):
+            if i not in self.read_set:
+                raise ValueError(f"read_set missing component {i}")
+            for source, slot in self.read_set[i]:
+                if not 0 <= source <= self.n_updatable:
+                    raise DimensionError(f"component {i} reads unknown source {source}")
+                if not 1 <= slot <= self.arity:
+                    raise DimensionError(f"component {i} uses slot {slot} > arity {self.arity}")
+        for slot, base in self.persistent_slots.items():
+            if base in self.persistent_slots:
+                raise ValueError(f"persistent slot {slot} chained onto persistent slot {base}")
+        for i in range(1, self.n_updatable + 1):
+            by_slot = {slot: src for src, slot in self.read_set[i]}
+            for slot, base in self.persistent_slots.items():
+                if slot in by_slot and by_slot.get(base) != by_slot[slot]:
+                    raise ValueError(f"component {i}: persistent slot {slot} must share its source with base slot {base}")
 
 
 @dataclass(frozen=True)

@@ -26,6 +26,7 @@ from .async_engine import (
     STOP_PREDICATE,
     STOP_QUIESCENCE,
     POLICY_ROUND_ROBIN,
+    AsyncMapping,
     AsyncSchedule,
     AsyncTrace,
     EngineView,
@@ -34,12 +35,50 @@ from .async_engine import (
 )
 from .errors import HorizonExhausted
 from .linalg import BlockVector
-from .parareal import _coarse_init_into, _u0_tensor, correct_into
+from .parareal import _coarse_init_into, _u0_tensor, correct_into, parareal_update
 
 FRESH_SLOT = 1
 REMEMBERED_SLOT = 2
 PERSISTENT_SLOTS = {REMEMBERED_SLOT: FRESH_SLOT}
 SNAPSHOT_LIMIT_BYTES = 1 << 30
+
+
+def async_parareal_mapping(coarse, fine, p: int) -> AsyncMapping:
+    """Two-slot mapping whose synchronous sweep is classic Parareal
+    (async_parareal.py:24-49): component i reads (i-1, FRESH) and
+    (i-1, REMEMBERED); REMEMBERED replays FRESH's previous reading. The
+    evaluation is ``parareal_update`` on the GPU."""
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+
+    def eval_fn(i: int, read_values: dict):
+        return parareal_update(coarse, fine, read_values[(i - 1, FRESH_SLOT)], read_values[(i - 1, REMEMBERED_SLOT)])
+
+    read_set = {i: ((i - 1, FRESH_SLOT), (i - 1, REMEMBERED_SLOT)) for i in range(1, p + 1)}
+    return AsyncMapping(n_updatable=p, arity=2, eval_fn=eval_fn, read_set=read_set,
+                        persistent_slots=dict(PERSISTENT_SLOTS), propagators=(coarse, fine))
+
+
+def simulate_async(mapping: AsyncMapping, init, schedule: AsyncSchedule, stop=None,
+                   record_snapshots: bool = True) -> AsyncTrace:
+    """Event loop of async_engine.py:238-365 for the Parareal mapping: runs
+    ``simulate_parareal_async`` (GPU state, retention buffers and evaluations).
+    ``init`` is a BlockVector / array / tensor with p + 1 rows."""
+    from .errors import DimensionError
+    if mapping.propagators is None:
+        raise NotImplementedError("simulate_async runs the Parareal mapping (async_parareal_mapping); "
+                                  "other fixed-point mappings are outside this build's hot path")
+    coarse, fine = mapping.propagators
+    p = mapping.n_updatable
+    t = init.tensor if isinstance(init, BlockVector) else init
+    t, _ = _device.as_device_tensor(t, coarse.device, coarse.dtype)
+    t = t.reshape(t.shape[0], -1) if t.dim() > 1 else t.reshape(1, -1)
+    if t.shape[0] != p + 1:
+        raise DimensionError(f"init has {t.shape[0]} blocks, expected {p + 1}")
+    if t.shape[1] != coarse.dim:
+        raise DimensionError(f"init blocks have dim {t.shape[1]}, expected {coarse.dim}")
+    return simulate_parareal_async(coarse, fine, t.contiguous().clone(), schedule, stop=stop,
+                                   record_snapshots=record_snapshots)
 
 
 def async_stop_check(worker_deltas, epsilon: float, drained: bool) -> bool:

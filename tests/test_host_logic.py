@@ -159,3 +159,22 @@ def test_package_inputs_match_the_oracle_bitwise():
         modes = I.modes_2d() if len(shape) == 2 else I.modes_3d()
         assert np.array_equal(I.sine_u0_nd(shape, modes, 2), H.sine_u0_nd(shape, modes, 2))
         assert np.array_equal(I.sine_u0(shape, seed=2), H.sine_u0_nd(shape, modes, 2).reshape(-1))
+
+
+def test_async_mapping_validation():
+    """reference async_engine.py:98-120."""
+    from paper_2110_10762_b200.async_engine import AsyncMapping
+    ok = AsyncMapping(2, 2, None, {1: ((0, 1), (0, 2)), 2: ((1, 1), (1, 2))}, {2: 1})
+    assert ok.n_updatable == 2
+    with pytest.raises(ValueError):
+        AsyncMapping(0, 1, None, {})
+    with pytest.raises(ValueError):
+        AsyncMapping(2, 1, None, {1: ((0, 1),)})
+    with pytest.raises(pb.DimensionError):
+        AsyncMapping(1, 1, None, {1: ((5, 1),)})
+    with pytest.raises(pb.DimensionError):
+        AsyncMapping(1, 1, None, {1: ((0, 2),)})
+    with pytest.raises(ValueError):
+        AsyncMapping(1, 3, None, {1: ((0, 1), (0, 2), (0, 3))}, {2: 1, 3: 2})
+    with pytest.raises(ValueError):
+        AsyncMapping(2, 2, None, {1: ((0, 1), (0, 2)), 2: ((1, 1), (0, 2))}, {2: 1})
