@@ -202,3 +202,31 @@ def test_large_ragged_sync_parareal_vs_long_double_truth(gpu, n, p, steps):
     assert tr.k_final == ref.k_final and tr.stop_reason == ref.stop_reason
     for k, it in enumerate(tr.iterates):
         assert rel_l2(it.data, ref.iterates[k]) < 1e-9, k
+
+
+@pytest.mark.parametrize("rule,n", [("backward-euler", 131_072), ("trapezoidal", 65_536), ("trapezoidal", 40_001)])
+def test_maximum_register_resident_sizes(gpu, rule, n):
+    """The largest 1-D grids the register-resident solver holds (4096 threads
+    x 32 points for backward Euler, x 16 for the trapezoidal rule; 16-CTA
+    clusters, generic coarse sweep) with Dirichlet forcing at both ends,
+    against the long-double oracle (measured <= 5.4e-13 relative L2, r = dt/h^2
+    up to 8.6e8); one point more is refused with
+    NotImplementedError (PINT_EUNSUPPORTED), never silently mis-solved."""
+    from oracle import heat_oracle as H
+    import torch
+    from oracle.truth import TruthTridiag1D
+    ivp = gpu.heat1d_system(n, 1.0, 0.5, -0.25, 0.0, 1.0)
+    fn = gpu.backward_euler_propagator if rule == "backward-euler" else gpu.trapezoidal_propagator
+    rng = np.random.default_rng(n)
+    states = rng.standard_normal((3, n))
+    for span, steps in ((1e-3, 4), (0.05, 1)):
+        prop = fn(ivp, span, steps)
+        got = prop.apply_batch(torch.tensor(states, device="cuda")).cpu().numpy()
+        a_d, a_o, c = H.heat1d_coeffs(n, 1.0, 0.5, -0.25)
+        want = TruthTridiag1D(n, a_d, a_o, c, span, steps, rule).apply_batch(states)
+        for b in range(3):
+            assert rel_l2(got[b], want[b]) < 1e-11, (span, steps, b, rel_l2(got[b], want[b]))
+    big = n + 1 if n in (131_072, 65_536) else None
+    if big:
+        with pytest.raises(NotImplementedError):
+            fn(gpu.heat1d_system(big, 1.0, 0.0, 0.0, 0.0, 1.0), 0.01, 1)
