@@ -230,3 +230,34 @@ def test_maximum_register_resident_sizes(gpu, rule, n):
     if big:
         with pytest.raises(NotImplementedError):
             fn(gpu.heat1d_system(big, 1.0, 0.0, 0.0, 0.0, 1.0), 0.01, 1)
+
+
+RAGGED_NS = (8_193, 12_289, 20_000, 33_000, 50_001, 70_001, 90_001, 110_001, 131_071)
+
+
+@pytest.mark.parametrize("n", RAGGED_NS)
+def test_ragged_layouts_apply_and_sweep(gpu, n):
+    """Every cluster-split class between 9 and 128 warps (padded warp counts,
+    1..16-CTA clusters, fused and generic coarse sweeps): F against the
+    long-double oracle, and one sync sweep against the oracle's restated
+    driver (same k, iterates within 1e-10: the coarse step has r = dt/h^2 up
+    to 4.3e9, where fp64 rounding alone reaches 1.5e-11)."""
+    import torch
+    from oracle import heat_oracle as H
+    from oracle.truth import TruthTridiag1D
+    ivp = gpu.heat1d_system(n, 1.0, 1.0, 2.0, 0.0, 1.0)
+    a_d, a_o, c = H.heat1d_coeffs(n, 1.0, 1.0, 2.0)
+    rng = np.random.default_rng(n)
+    u = rng.standard_normal((2, n))
+    fine = gpu.backward_euler_propagator(ivp, 0.25, 3)
+    coarse = gpu.backward_euler_propagator(ivp, 0.25, 1)
+    got = fine.apply_batch(torch.tensor(u, device="cuda")).cpu().numpy()
+    F = TruthTridiag1D(n, a_d, a_o, c, 0.25, 3)
+    G = TruthTridiag1D(n, a_d, a_o, c, 0.25, 1)
+    want = F.apply_batch(u)
+    assert rel_l2(got[0], want[0]) < 1e-11 and rel_l2(got[1], want[1]) < 1e-11
+    tr = gpu.run_parareal(coarse, fine, u[0], 4, 0.0, k_max=2, record_iterates=True)
+    ref = H.run_parareal(G, F, u[0], 4, 0.0, k_max=2)
+    assert tr.k_final == ref.k_final == 2
+    for k, it in enumerate(tr.iterates):
+        assert rel_l2(it.data, ref.iterates[k]) < 1e-10, k
