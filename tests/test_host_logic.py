@@ -178,3 +178,10 @@ def test_async_mapping_validation():
         AsyncMapping(1, 3, None, {1: ((0, 1), (0, 2), (0, 3))}, {2: 1, 3: 2})
     with pytest.raises(ValueError):
         AsyncMapping(2, 2, None, {1: ((0, 1), (0, 2)), 2: ((1, 1), (0, 2))}, {2: 1})
+
+
+def test_simulate_async_needs_the_parareal_mapping():
+    from paper_2110_10762_b200.async_engine import AsyncMapping
+    m = AsyncMapping(1, 1, lambda i, r: r[(0, 1)], {1: ((0, 1),)})
+    with pytest.raises(NotImplementedError):
+        pb.simulate_async(m, np.zeros((2, 3)), pb.AsyncSchedule(seed=0))
