@@ -184,4 +184,4 @@ def test_simulate_async_needs_the_parareal_mapping():
     from paper_2110_10762_b200.async_engine import AsyncMapping
     m = AsyncMapping(1, 1, lambda i, r: r[(0, 1)], {1: ((0, 1),)})
     with pytest.raises(NotImplementedError):
-        pb.simulate_async(m, np.zeros((2, 3)), pb.AsyncSchedule(seed=0))
+        pb.simulate_async(m, np.zeros((2, 3)), pb.AsyncSchedule(seed=0, delay_bound=0))
