@@ -261,3 +261,27 @@ def test_ragged_layouts_apply_and_sweep(gpu, n):
     assert tr.k_final == ref.k_final == 2
     for k, it in enumerate(tr.iterates):
         assert rel_l2(it.data, ref.iterates[k]) < 1e-10, k
+
+
+@pytest.mark.parametrize("n,p", [(50_001, 24), (65_536, 16)])
+def test_trapezoidal_fine_backward_euler_coarse_large(gpu, n, p):
+    """The reference fixtures' pairing (trapezoidal F, backward-Euler G,
+    conftest.py:16-32) at C2-class sizes with Dirichlet forcing: the coarse
+    operator takes the 16-point register layout of the trapezoidal fine one;
+    sync Parareal against the long-double oracle driving the restated
+    reference algorithm (same k and stop reason, iterates within 1e-9)."""
+    from oracle import heat_oracle as H
+    from oracle.truth import TruthTridiag1D
+    from paper_2110_10762_b200.inputs import sine_u0_1d
+    ivp = gpu.heat1d_system(n, 1.0, 0.3, -0.2, 0.0, 1.0)
+    fine = gpu.trapezoidal_propagator(ivp, 1 / p, 20)
+    coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
+    u0 = sine_u0_1d(n, 16, 7)
+    tr = gpu.run_parareal(coarse, fine, u0, p, 1e-9, k_max=5, record_iterates=True)
+    a_d, a_o, c = H.heat1d_coeffs(n, 1.0, 0.3, -0.2)
+    F = TruthTridiag1D(n, a_d, a_o, c, 1 / p, 20, "trapezoidal")
+    G = TruthTridiag1D(n, a_d, a_o, c, 1 / p, 1)
+    ref = H.run_parareal(G, F, u0, p, 1e-9, k_max=5)
+    assert tr.k_final == ref.k_final and tr.stop_reason == ref.stop_reason
+    for k, it in enumerate(tr.iterates):
+        assert rel_l2(it.data, ref.iterates[k]) < 1e-9, k
