@@ -115,15 +115,17 @@ def test_device_async_quiescence_is_the_sequential_solution(gpu, delay):
     assert res.kappa >= 1 and res.activations >= p
 
 
-@pytest.mark.parametrize("n,p,domains", [(65537, 24, 1), (100_000, 20, 2)])
-def test_device_async_ragged_large_grid_quiescence(gpu, n, p, domains):
+@pytest.mark.parametrize("n,p,domains,rule", [(65537, 24, 1, "be"), (100_000, 20, 2, "be"), (40_001, 16, 2, "cn")])
+def test_device_async_ragged_large_grid_quiescence(gpu, n, p, domains, rule):
     """Ragged C2-scale grids (10- and 14-CTA clusters, padded warps, tail
-    chunks): the persistent runtime still quiesces on the sequential fine
-    solution bitwise."""
+    chunks; trapezoidal F with forcing on the 16-point layout): the
+    persistent runtime still quiesces on the sequential fine solution
+    bitwise."""
     from paper_2110_10762_b200.inputs import sine_u0_1d
     u0 = sine_u0_1d(n, 16, 5)
-    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
-    fine = gpu.backward_euler_propagator(ivp, 1 / p, 10)
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0) if rule == "be" else gpu.heat1d_system(n, 1.0, 0.4, 0.1, 0.0, 1.0)
+    fn = gpu.backward_euler_propagator if rule == "be" else gpu.trapezoidal_propagator
+    fine = fn(ivp, 1 / p, 10)
     coarse = gpu.backward_euler_propagator(ivp, 1 / p, 1)
     seq = gpu.sequential_fine_solve(fine, u0, p).data
     res = gpu.run_async_parareal_device(coarse, fine, u0, p, None, delay_frac=0.1, seed=n, domains=domains)
