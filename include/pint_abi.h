@@ -26,6 +26,13 @@
  *                               simulate_async event loop, async_engine.py:238-365)
  *   pint_async_run_traced   <- + AsyncTrace / UpdateRecord  async_engine.py:122-190
  *                              (audited as validate_schedule, async_engine.py:402-459)
+ *   pint_correct_chain      <- one step of the coarse chain of run_parareal
+ *                              parareal.py:119-127 (F-only decided from the
+ *                              predecessor's delta, G(old) cache refreshed)
+ *   pint_shared_*, pint_ipc_*, pint_mailbox_*, pint_board_*
+ *                           <- the predecessor reads of async_parareal.py:24-49
+ *                              and the drained stop of async_engine.py:287-291
+ *                              across processes/GPUs (async_mp.py)
  *   pint_async_domain_*     <- run_async_parareal across GPUs (one domain of
  *                              contiguous slices per GPU; the slice-boundary
  *                              state is pushed to the next GPU by P2P stores;
@@ -215,6 +222,61 @@ int pint_sync_sweep_chain(pint_op *coarse, const void *prev, void *next,
                           const void *fv, void *gcache, int64_t k, int64_t p,
                           double *deltas_dev, int32_t *nonfinite_dev,
                           void *stream);
+
+/*
+ * One step of the serial coarse chain (generic sweep), slice i:
+ *   f_only := (f_only && *f_only) || (fonly_delta_dev && *fonly_delta_dev == 0)
+ *             (array_equal(fresh, old) <=> the predecessor's delta is 0)
+ *   out     = f_only ? f : (gnew + f) - gcache          (parareal.py:34-36)
+ *   gcache <- gnew                                      (next sweep's G(old))
+ *   *delta_dev = max(*delta_dev, max |out - prev|)      (caller zeroes it per sweep)
+ * out may alias prev or f (elementwise, read before write). One launch.
+ */
+int pint_correct_chain(pint_ctx *ctx, int32_t dtype, int64_t dim, const void *gnew,
+                       const void *f, void *gcache, const void *prev, void *out,
+                       const uint8_t *f_only, const double *fonly_delta_dev,
+                       double *delta_dev, int32_t *nonfinite_dev, void *stream);
+
+/*
+ * Cross-process exchange for the multi-GPU asynchronous runtime (async_mp.py).
+ * pint_shared_alloc: zeroed device memory that can be exported;
+ * pint_ipc_export / pint_ipc_open / pint_ipc_close: 64-byte CUDA IPC handles.
+ */
+int pint_shared_alloc(pint_ctx *ctx, int64_t bytes, void **dev_ptr);
+int pint_shared_free(pint_ctx *ctx, void *dev_ptr);
+int pint_ipc_export(pint_ctx *ctx, void *dev_ptr, uint8_t *handle64);
+int pint_ipc_open(pint_ctx *ctx, const uint8_t *handle64, void **dev_ptr);
+int pint_ipc_close(pint_ctx *ctx, void *dev_ptr);
+
+/*
+ * Push `bytes` from src into dst (any device address, e.g. a peer's mailbox
+ * slot opened through IPC) with SM stores, then publish: *ver = version with a
+ * system-scope release once every CTA's stores are fenced. done_ctr: a zeroed
+ * device uint32 owned by the calling stream. 16-byte aligned rows.
+ */
+int pint_mailbox_push(pint_ctx *ctx, void *dst, const void *src, int64_t bytes, int64_t *ver,
+                      int64_t version, uint32_t *done_ctr, void *stream);
+
+/*
+ * Seqlock read of the freshest published version v of a ring of nslots
+ * slots (slot_bytes apart) guarded by *ver: dst <- slot v % nslots,
+ * *v_out = v, *torn = 1 if the producer may have started overwriting the
+ * slot during the copy (version advanced by more than nslots - 2). vsel is a
+ * device int64 scratch word of the stream.
+ */
+int pint_mailbox_read(pint_ctx *ctx, const void *ring, int64_t slot_bytes, int64_t nslots,
+                      const int64_t *ver, void *dst, int64_t bytes, int64_t *vsel,
+                      int64_t *v_out, int32_t *torn, void *stream);
+
+/*
+ * Status boards: slot = 8 int64 {seq, w0..w6}; post writes seq+1, the seven
+ * words, seq+2 (system-scope release); read snapshots nslots slots with
+ * acquire loads until both sequence reads agree (seq -1 if a slot never
+ * settles) into out_dev (nslots x 8).
+ */
+int pint_board_post(pint_ctx *ctx, int64_t *slot, int64_t seq, const int64_t *words7, void *stream);
+int pint_board_read(pint_ctx *ctx, const int64_t *board, int32_t nslots, int64_t *out_dev,
+                    void *stream);
 
 /*
  * Asynchronous Parareal with real concurrency on one GPU (persistent launch;

@@ -37,25 +37,37 @@ int thomas_ld_propagate(int64_t n, int64_t nbatch, double *states, double Dd, do
     inv[i] = 1.0L / piv;
     cp[i] = E * inv[i];
   }
-  for (int64_t b = 0; b < nbatch; ++b) {
-    double *s = states + b * n;
-    for (int64_t i = 0; i < n; ++i) x[i] = s[i];
-    for (int64_t k = 0; k < steps; ++k) {
-      if (cn) {
-        for (int64_t i = 0; i < n; ++i) {
-          ld v = (ld)two_minus_d * x[i];
-          if (i > 0) v -= E * x[i - 1];
-          if (i < n - 1) v -= E * x[i + 1];
-          y[i] = v;
+  /* independent slices: one per OpenMP thread (private work rows) */
+  int bad = 0;
+#pragma omp parallel reduction(| : bad)
+  {
+    ld *xt = (ld *)malloc(sizeof(ld) * n), *yt = (ld *)malloc(sizeof(ld) * n);
+    if (!xt || !yt) bad = 1;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nbatch; ++b) {
+      if (!xt || !yt) continue;
+      double *s = states + b * n;
+      for (int64_t i = 0; i < n; ++i) xt[i] = s[i];
+      for (int64_t k = 0; k < steps; ++k) {
+        if (cn) {
+          for (int64_t i = 0; i < n; ++i) {
+            ld v = (ld)two_minus_d * xt[i];
+            if (i > 0) v -= E * xt[i - 1];
+            if (i < n - 1) v -= E * xt[i + 1];
+            yt[i] = v;
+          }
+          for (int64_t i = 0; i < n; ++i) xt[i] = yt[i];
         }
-        for (int64_t i = 0; i < n; ++i) x[i] = y[i];
+        xt[0] += f_first;
+        if (n > 1) xt[n - 1] += f_last;
+        solve(n, D, E, cp, inv, xt);
       }
-      x[0] += f_first;
-      if (n > 1) x[n - 1] += f_last;
-      solve(n, D, E, cp, inv, x);
+      for (int64_t i = 0; i < n; ++i) s[i] = (double)xt[i];
     }
-    for (int64_t i = 0; i < n; ++i) s[i] = (double)x[i];
+    free(xt);
+    free(yt);
   }
+  if (bad) { free(cp); free(inv); free(x); free(y); return 1; }
   free(cp); free(inv); free(x); free(y);
   return 0;
 }

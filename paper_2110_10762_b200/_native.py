@@ -94,6 +94,18 @@ SIGNATURES = {
                                        ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p]),
     "pint_max_reduce": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p]),
     "pint_equal_flag": (c_int, [c_void_p, c_i32, c_i64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pint_correct_chain": (c_int, [c_void_p, c_i32, c_i64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pint_shared_alloc": (c_int, [c_void_p, c_i64, ctypes.POINTER(c_void_p)]),
+    "pint_shared_free": (c_int, [c_void_p, c_void_p]),
+    "pint_ipc_export": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "pint_ipc_open": (c_int, [c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
+    "pint_ipc_close": (c_int, [c_void_p, c_void_p]),
+    "pint_mailbox_push": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
+    "pint_mailbox_read": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p, c_i64, c_void_p, c_void_p,
+                                  c_void_p, c_void_p]),
+    "pint_board_post": (c_int, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "pint_board_read": (c_int, [c_void_p, c_void_p, c_i32, c_void_p, c_void_p]),
     "pint_tri1d_plan_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 

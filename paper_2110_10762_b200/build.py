@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libpint_b200.so")
 STAMP = LIB + ".srchash"
 
-SOURCES = ["abi.cu", "tri1d.cu", "async_rt.cu", "correct.cu", "stencil.cu", "stencil_wave.cu", "stencil3d.cu", "cg.cu", "spectral.cu", "tc_xform.cu"]
+SOURCES = ["abi.cu", "tri1d.cu", "async_rt.cu", "correct.cu", "stencil.cu", "stencil_wave.cu", "stencil3d.cu", "cg.cu", "spectral.cu", "tc_xform.cu", "mailbox.cu"]
 HEADERS = ["pint_internal.cuh", "tri1d_device.cuh", os.path.join("..", "..", "include", "pint_abi.h")]
 
 NVCC_FLAGS = [

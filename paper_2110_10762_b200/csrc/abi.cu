@@ -16,19 +16,7 @@ void pint_check_cuda(cudaError_t e, const char *what) {
 
 template <typename F>
 static int guarded(pint_ctx *ctx, F &&fn) {
-  try {
-    fn();
-    return PINT_OK;
-  } catch (const PintError &e) {
-    if (ctx) {
-      ctx->last_error = e.msg;
-      ctx->last_value = e.value;
-    }
-    return e.code;
-  } catch (const std::exception &e) {
-    if (ctx) ctx->last_error = e.what();
-    return PINT_ECUDA;
-  }
+  return pint_guarded(ctx, static_cast<F &&>(fn));
 }
 
 static thread_local std::string g_orphan_error;
@@ -245,6 +233,20 @@ int pint_sync_sweep_chain(pint_op *coarse, const void *prev, void *next, const v
     if (!is_tri1d(coarse)) pint_throw(PINT_EUNSUPPORTED, "fused sweep is implemented for 1-D implicit coarse operators");
     tri1d_sweep(coarse, (const double *)prev, (double *)next, (const double *)fv, (double *)gcache, k, p,
                 deltas_dev, nonfinite_dev, (cudaStream_t)stream, 1);
+  });
+}
+
+int pint_correct_chain(pint_ctx *ctx, int32_t dtype, int64_t dim, const void *gnew, const void *f, void *gcache,
+                       const void *prev, void *out, const uint8_t *f_only, const double *fonly_delta_dev,
+                       double *delta_dev, int32_t *nonfinite_dev, void *stream) {
+  if (!ctx) return PINT_EARG;
+  return guarded(ctx, [&] {
+    if (dtype != PINT_F32 && dtype != PINT_F64) pint_throw(PINT_EARG, "dtype must be PINT_F32 or PINT_F64");
+    if (dim < 0) pint_throw(PINT_EDIM, "negative size");
+    if (dim == 0) return;
+    if (!gnew || !f || !gcache || !out) pint_throw(PINT_EARG, "null state pointer");
+    correct_chain_launch(dtype, dim, gnew, f, gcache, prev, out, f_only, fonly_delta_dev, delta_dev, nonfinite_dev,
+                         (cudaStream_t)stream);
   });
 }
 

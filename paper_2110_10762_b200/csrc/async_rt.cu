@@ -297,11 +297,21 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
         break;
       }
       ctl[0] = slot;
-      ctl_broadcast(ctl, CL, 1);
+      if (slot >= 0) {
+        // acquire the previous owner's release of this slice (its busy
+        // unlock follows its publish), then read the slice's bookkeeping once
+        // for the whole cluster
+        __threadfence();
+        ctl[3] = *(volatile long long *)(D.ver + slot);
+        ctl[4] = *(volatile long long *)(D.vrem + slot);
+        ctl[5] = *(volatile long long *)(D.counts + slot);
+      }
+      ctl_broadcast(ctl, CL, 6);
     }
     cluster.sync();
     const long long r = ctl[0];
     if (r < 0) break;
+    const long long vi = ctl[3], vr = ctl[4], cnt = ctl[5];
     const long long gi = D.lo - 1 + r;  // global slice index
 
     // ---- F(remembered)
@@ -311,7 +321,7 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
     store_chunk<CH>(x, sF, N, cF.t);
     if (S.delay_frac > 0.0 && rank == 0 && threadIdx.x == 0) {
       const unsigned long long tF = globaltimer() - tf0;
-      const unsigned long long hs = mix64(S.seed ^ ((unsigned long long)gi << 32) ^ (unsigned long long)D.counts[r]);
+      const unsigned long long hs = mix64(S.seed ^ ((unsigned long long)gi << 32) ^ (unsigned long long)cnt);
       const double u = (double)(hs >> 11) * (1.0 / 9007199254740992.0);
       const unsigned long long until = globaltimer() + (unsigned long long)(u * S.delay_frac * (double)tF);
       while (globaltimer() < until) __nanosleep(1000);
@@ -327,8 +337,11 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
       cluster.sync();
       v = ctl[1];
       load_chunk_cg<CH>(x, D.ring + ((size_t)(r - 1) * R + (size_t)(v % R)) * N, N, cF.t);
-      __syncthreads();
+      // every CTA's slot loads are ordered before the version re-read
+      // (barrier.cluster arrive.release / wait.acquire, then a fence)
+      cluster.sync();
       if (rank == 0 && threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
         const long long v2 = ld_acquire_sys(D.ver + r - 1);
         ctl[2] = (v2 <= v + R - 2) ? 1 : 0;
         if (!ctl[2]) atomicAdd((unsigned long long *)D.retries, 1ull);
@@ -337,7 +350,6 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
       cluster.sync();
       if (ctl[2]) break;
     }
-    const long long vr = D.vrem[r];
     // bitwise comparison with the remembered reading (array_equal semantics)
     double mism = 0.0;
 #pragma unroll
@@ -352,7 +364,6 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
     const bool fonly = (v == vr) || (anymism == 0.0);
 
     // ---- correction, delta, publish into the next ring slot (+ the next domain's mailbox)
-    const long long vi = D.ver[r];
     const double *cur = D.ring + ((size_t)r * R + (size_t)(vi % R)) * N + base;
     double *dst = D.ring + ((size_t)r * R + (size_t)((vi + 1) % R)) * N + base;
     double *peer = (r == nloc && D.next_ring) ? D.next_ring + (size_t)((vi + 1) % R) * N + base : nullptr;

@@ -30,6 +30,25 @@ struct PintError {
 void pint_check_cuda(cudaError_t e, const char *what);
 #define PINT_CUDA(call) pint_check_cuda((call), #call)
 
+// Run fn, converting a PintError / std::exception into a status code and the
+// context's last-error message (the ABI edge of every entry point).
+template <typename F>
+inline int pint_guarded(pint_ctx *ctx, F &&fn) {
+  try {
+    fn();
+    return PINT_OK;
+  } catch (const PintError &e) {
+    if (ctx) {
+      ctx->last_error = e.msg;
+      ctx->last_value = e.value;
+    }
+    return e.code;
+  } catch (const std::exception &e) {
+    if (ctx) ctx->last_error = e.what();
+    return PINT_ECUDA;
+  }
+}
+
 // ------------------------------------------------------------ 1-D tridiagonal
 
 // Uniform (kernel-parameter) factors of one chunk class.
@@ -135,6 +154,9 @@ void correct_launch(int dtype, int64_t dim, int64_t nbatch, const void *gnew,
                     const void *f, const void *gold, const void *prev, void *out,
                     const uint8_t *f_only, double *delta, int32_t *nonfinite,
                     cudaStream_t s);
+void correct_chain_launch(int dtype, int64_t dim, const void *gnew, const void *f, void *gcache, const void *prev,
+                          void *out, const uint8_t *f_only, const double *fonly_delta, double *delta,
+                          int32_t *nonfinite, cudaStream_t s);
 void max_reduce_launch(const double *d, int64_t lo, int64_t hi, double *out,
                        cudaStream_t s);
 void equal_launch(int dtype, int64_t dim, const void *a, const void *b, uint8_t *eq, cudaStream_t s);

@@ -83,7 +83,7 @@ fe_block_kernel(const StencilArgs<T> a) {
         T nb = src[i - 1] + src[i + 1];
         if (DIM >= 2) nb += src[i - LX] + src[i + LX];
         if (DIM >= 3) nb += src[i - LX * LY] + src[i + LX * LY];
-        v = u + a.r * (nb - c * u);
+        v = fma(a.r, fma(-c, u, nb), u);  // pinned expression (oracle/stencil_nd.c)
       }
       dst[i] = v;
     }

@@ -110,7 +110,7 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
         const T rr = (c == CPT2 - 1) ? right : prv[L][c + 1];
         const T ctr = prv[L][c];
         const T nb = (l + rr) + (pp[L][c] + cur[L][c]);
-        v[c] = (rin && colin[c]) ? ctr + r * (nb - four * ctr) : T(0);
+        v[c] = (rin && colin[c]) ? fma(r, fma(-four, ctr, nb), ctr) : T(0);
       }
       if (L + 1 < S) {
 #pragma unroll
@@ -328,7 +328,7 @@ __device__ __forceinline__ void plane3(T (&cur)[S][CPT3], T (&prv)[S][CPT3], T (
         const T xl = (c == 0) ? left : prv[L][c - 1];
         const T xr = (c == CPT3 - 1) ? right : prv[L][c + 1];
         const T nb = ((xl + xr) + (upv[c] + dnv[c])) + (pp[L][c] + cur[L][c]);
-        v[c] = (rin && colin[c]) ? ctr + r * (nb - six * ctr) : T(0);
+        v[c] = (rin && colin[c]) ? fma(r, fma(-six, ctr, nb), ctr) : T(0);
       }
     }
     if (L + 1 < S) {

@@ -2,8 +2,11 @@
 
 The interface states lambda_0..lambda_p are stored as one (P+1) x dim
 row-major, slice-major array — here a device tensor in HBM. ``.data`` keeps
-the reference's contract (a numpy array) by copying to the host on demand;
-``.tensor`` is the device view used by the hot path.
+the reference's read contract (a numpy array) through a host copy made on
+demand; that copy is READ-ONLY (writing into it raises instead of being
+silently lost — the device tensor is the storage), and it is refreshed
+whenever the tensor has been modified in place since. ``.tensor`` is the
+device view used by the hot path; mutate state through it.
 """
 from __future__ import annotations
 
@@ -14,7 +17,7 @@ from .errors import DimensionError
 
 
 class BlockVector:
-    __slots__ = ("tensor", "_host")
+    __slots__ = ("tensor", "_host", "_host_version")
 
     def __init__(self, data, check_finite: bool = True):
         if isinstance(data, torch.Tensor):
@@ -28,16 +31,31 @@ class BlockVector:
             raise ValueError("block entries must be finite")
         self.tensor = t
         self._host = None
+        self._host_version = -1
 
     @classmethod
     def from_blocks(cls, blocks) -> "BlockVector":
         return cls(np.stack([np.asarray(b, dtype=float) for b in blocks]))
 
+    @classmethod
+    def from_flat(cls, flat, n_blocks: int) -> "BlockVector":
+        """Reshape a flat vector into ``n_blocks`` equal blocks (linalg.py:96)."""
+        a = np.asarray(flat, dtype=float).reshape(-1)
+        if n_blocks <= 0 or a.size % n_blocks:
+            raise DimensionError(f"cannot split {a.size} entries into {n_blocks} blocks")
+        return cls(a.reshape(n_blocks, -1))
+
     @property
     def data(self) -> np.ndarray:
-        """Host copy (numpy), as the reference's ``BlockVector.data``."""
-        if self._host is None:
-            self._host = self.tensor.detach().to("cpu").numpy()
+        """Read-only host copy (numpy) of the blocks (the reference's
+        ``BlockVector.data`` for reading); refreshed after in-place changes of
+        the device tensor."""
+        ver = self.tensor._version
+        if self._host is None or self._host_version != ver:
+            h = self.tensor.detach().to("cpu").numpy()
+            h.flags.writeable = False
+            self._host = h
+            self._host_version = ver
         return self._host
 
     @property

@@ -56,6 +56,19 @@ def correct_into(ctx_prop, gnew, f, gold, prev, out, f_only, delta, nonfinite, n
     _native.check(rc, _ctx(ctx_prop), "pint_correct")
 
 
+def correct_chain_into(ctx_prop, gnew, f, gcache, prev, out, fonly_delta, delta, nonfinite, f_only=None) -> None:
+    """pint_correct_chain: one coarse-chain step of the generic sweep (F-only
+    decided on the device from the predecessor's delta, G(old) cache
+    refreshed in place, delta accumulated into a slot zeroed per sweep)."""
+    lib = _native.load_library()
+    dtype = _native.PINT_F64 if out.dtype == torch.float64 else _native.PINT_F32
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None else 0)  # noqa: E731
+    rc = lib.pint_correct_chain(_ctx(ctx_prop), dtype, int(out.shape[-1]), ptr(gnew), ptr(f), ptr(gcache), ptr(prev),
+                                ptr(out), ptr(f_only), ptr(fonly_delta), ptr(delta), ptr(nonfinite),
+                                _stream(ctx_prop))
+    _native.check(rc, _ctx(ctx_prop), "pint_correct_chain")
+
+
 def parareal_update(coarse, fine, fresh_prev, old_prev):
     """One interface-state correction from two predecessor readings
     (parareal.py:25-36). Inputs may be numpy arrays or device tensors; the
@@ -179,7 +192,6 @@ class SyncEngine:
         self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
         self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.fonly = torch.zeros(p + 1, dtype=torch.bool, device=dev)  # generic sweep: per-slice F-only mask
         self.host = torch.zeros(2, dtype=torch.float64).pin_memory() if torch.cuda.is_available() else None
         self.fused = coarse.is_tridiagonal and bool(coarse.info.fused_sweep)
         self.prev = self.lam_a
@@ -501,22 +513,24 @@ class SyncEngine:
 
     def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
         """Coarse chain + correction for coarse operators without a fused
-        sweep kernel (CG coarse in 2-D/3-D): same values, one launch per slice."""
+        sweep kernel (2-D/3-D direct or CG coarse): same values, two launches
+        per slice (G, then pint_correct_chain: the F-only branch from the
+        predecessor's delta, the G(old) cache refreshed in place)."""
         p, prev = self.p, self.prev
         if not chain_in:
             nxt[k - 1].copy_(prev[k - 1])
-            self.deltas[k - 1] = 0.0
-        g = torch.empty(1, self.fine.dim, dtype=self.fine.dtype, device=nxt.device)
-        if not chain_in:
-            self.fonly[k] = True
+        # slice k-1 is frozen (delta 0 => F-only for slice k) unless its new value came in on the chain
+        self.deltas[k if chain_in else k - 1:].zero_()
+        g = self._gbuf(nxt)
         for i in range(k, p + 1):
             self.coarse.apply_ptr(nxt[i - 1].data_ptr(), g.data_ptr(), 1, self.fine.dim)
-            if chain_in or i > k:
-                # F-only branch iff slice i-1 did not move (delta 0), decided on the device
-                torch.eq(self.deltas[i - 1:i], 0.0, out=self.fonly[i:i + 1])
-            correct_into(self.fine, g, self.fv[i:i + 1], self.gcache[i:i + 1], prev[i:i + 1], nxt[i:i + 1],
-                         self.fonly[i:i + 1], self.deltas[i:i + 1], self.flag, 1)
-            self.gcache[i].copy_(g[0])
+            correct_chain_into(self.fine, g[0], self.fv[i], self.gcache[i], prev[i], nxt[i], self.deltas[i - 1:i],
+                               self.deltas[i:i + 1], self.flag)
+
+    def _gbuf(self, like: torch.Tensor) -> torch.Tensor:
+        if getattr(self, "_g", None) is None or self._g.device != like.device:
+            self._g = torch.empty(1, self.fine.dim, dtype=self.fine.dtype, device=like.device)
+        return self._g
 
     def read_delta(self) -> float:
         """Host read of the sweep's delta (the one sync per sweep)."""
@@ -556,7 +570,6 @@ class LeanSyncEngine:
         self.deltas = torch.zeros(p + 1, dtype=torch.float64, device=dev)
         self.dmax = torch.zeros(1, dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.fonly = torch.zeros(p + 1, dtype=torch.bool, device=dev)
         self.prev = self.lam_a
         self.lib = _native.load_library()
 
@@ -570,7 +583,6 @@ class LeanSyncEngine:
         if nxt is not lam:
             raise ValueError("the lean engine updates its iterate in place")
         self.deltas.zero_()
-        self.fonly[k] = True  # slice k-1 is frozen: F-only for slice k
         a = k
         while a <= p:
             b = min(p, a + self.chunk - 1)
@@ -585,13 +597,10 @@ class LeanSyncEngine:
                 self.saved[0].copy_(lam[b])
             for i in range(a, b + 1):
                 self.coarse.apply_ptr(lam[i - 1].data_ptr(), self.g.data_ptr(), 1, n)
-                if i > k:
-                    torch.eq(self.deltas[i - 1:i], 0.0, out=self.fonly[i:i + 1])
-                row = self.fv[i - a:i - a + 1]
-                correct_into(self.fine, self.g, row, self.gcache[i:i + 1], lam[i:i + 1], row,
-                             self.fonly[i:i + 1], self.deltas[i:i + 1], self.flag, 1)
-                self.gcache[i].copy_(self.g[0])
-                lam[i].copy_(row[0])
+                # in place: lam[i] is read (delta) before it is overwritten, element by element;
+                # F-only iff slice i-1 did not move (its delta of this sweep is 0; slice k-1 is frozen)
+                correct_chain_into(self.fine, self.g[0], self.fv[i - a], self.gcache[i], lam[i], lam[i],
+                                   self.deltas[i - 1:i], self.deltas[i:i + 1], self.flag)
             a = b + 1
         rc = self.lib.pint_max_reduce(_ctx(self.fine), ctypes.c_void_p(self.deltas.data_ptr()), k - 1, p + 1,
                                       ctypes.c_void_p(self.dmax.data_ptr()), _stream(self.fine))
@@ -643,30 +652,33 @@ def run_parareal(coarse, fine, u0, p: int, epsilon: float, k_max: int | None = N
     slice_deltas: list = []
     stop_reason = STOP_KMAX
     k = 0
-    while k < cap:
-        k += 1
-        nxt = eng.lam_b if eng.prev is eng.lam_a else eng.lam_a
-        if record_iterates and nxt is not eng.prev:
-            nxt.copy_(eng.prev)
-        # sweep k+1's first F starts while this sweep's chain and the host's
-        # delta read finish (discarded if this sweep stops the iteration)
-        eng.sweep(k, nxt, speculate=k < cap)
-        delta = eng.read_delta()
-        deltas.append(delta)
-        slice_deltas.append(eng.deltas.to("cpu").numpy().copy())
-        if record_iterates:
-            iterates.append(BlockVector(nxt.clone(), check_finite=False))
-        if delta < epsilon:
-            stop_reason = STOP_THRESHOLD
-            break
-        if k == p:
-            stop_reason = STOP_EXACT
-            break
-        if k == cap:
-            stop_reason = STOP_KMAX
-            break
-    if hasattr(eng, "finish"):
-        eng.finish()
+    try:
+        while k < cap:
+            k += 1
+            nxt = eng.lam_b if eng.prev is eng.lam_a else eng.lam_a
+            if record_iterates and nxt is not eng.prev:
+                nxt.copy_(eng.prev)
+            # sweep k+1's first F starts while this sweep's chain and the host's
+            # delta read finish (discarded if this sweep stops the iteration)
+            eng.sweep(k, nxt, speculate=k < cap)
+            delta = eng.read_delta()
+            deltas.append(delta)
+            slice_deltas.append(eng.deltas.to("cpu").numpy().copy())
+            if record_iterates:
+                iterates.append(BlockVector(nxt.clone(), check_finite=False))
+            if delta < epsilon:
+                stop_reason = STOP_THRESHOLD
+                break
+            if k == p:
+                stop_reason = STOP_EXACT
+                break
+            if k == cap:
+                stop_reason = STOP_KMAX
+                break
+    finally:
+        # a speculative F may still be writing engine buffers (also on an exception)
+        if hasattr(eng, "finish"):
+            eng.finish()
     # the engine is not reused: hand its iterate over (lean) or copy it out
     final = BlockVector(eng.prev if lean else eng.prev.clone(), check_finite=False)
     if not record_iterates:
