@@ -187,19 +187,46 @@ def ncu_traffic() -> float | None:
 
 
 # -------------------------------------------------------------- reference arm
+def _cpu_pool(cores: int):
+    import multiprocessing as mp
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    return mp.get_context("fork").Pool(cores)
+
+
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference's fine propagation restated on the host (oracle port:
+    LAPACK gttrs per backward-Euler step, the reference's coefficients), all
+    host cores, one slice per process. Every step is one bounded sample of
+    the C2 workload: `cores` slice applications of F (1000 steps, N = 65,536)
+    run concurrently; W untimed warm-up samples, then exactly K timed ones."""
     if rank != 0:
         return
-    cb = cpu_baseline(target_s=max(5.0, 90.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    for _ in range(args.warmup):
-        pass
-    for _ in range(args.steps):
-        vals.append(cb["value"])
-    value = float(np.mean(vals))
+    cores = os.cpu_count() or 1
+    pool = _cpu_pool(cores)
+    try:
+        def sample(seed0):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker, [(N_POINTS, FINE_STEPS, 1, seed0 + s) for s in range(cores)])
+            return time.perf_counter() - t0, sum(r[1] for r in res)
+
+        for w in range(args.warmup):
+            sample(1000 * (w + 1))
+        secs, upd = [], 0
+        for k in range(args.steps):
+            t, u = sample(k)
+            secs.append(t)
+            upd += u
+    finally:
+        pool.close()
+        pool.join()
+    value = upd / sum(secs) / 1e9
+    desc = (f"each step: {cores} concurrent slice applications of F (1000 BE steps, N={N_POINTS}; "
+            f"oracle/heat_oracle.py Tridiag1D = LAPACK gttrs per step), one per process")
+    cb = {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc, "cpu": _cpu_model()}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(world), "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -272,32 +299,39 @@ def run_ours(args, rank: int, world: int) -> None:
     ms_step = dist_rt.max_over_ranks(ms_step_local) if world > 1 else ms_step_local
     value = updates_per_step * world / (ms_step * 1e-3) / 1e9
 
-    # end-to-end through the public API with host buffers (pinned H2D of the
-    # iterate, sweep, D2H of the new iterate + the delta), every step
+    # end-to-end through the reference's public API with host buffers: one
+    # full sweep pb.parareal_iterate (parareal.py:66-76) from a pinned host
+    # iterate to a pinned host result, every step (H2D of the iterate, the
+    # sweep, D2H of the new iterate inside the timed region)
     host_in = torch.from_numpy(base.cpu().numpy()).pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
+    lam_host = pb.BlockVector(host_in, check_finite=False)
     e2e_ms = []
     for it in range(args.warmup + args.steps):
-        gcache.copy_(base_g)
         flush.fill_(1.0)
         if world > 1:
             dist_rt.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if world == 1:
-            # public host-buffer sweep: per-chunk uploads/downloads overlapped with compute
-            eng.prev = eng.lam_b
-            d = eng.sweep_host(1, host_in, host_out, graph=True)
+            res = pb.parareal_iterate(coarse, fine, lam_host, out=host_out)
         else:
             eng.lam_a.copy_(host_in, non_blocking=True)
             eng.prev = eng.lam_a
             eng.sweep(1, nxt)
-            d = eng.read_delta()
+            eng.read_delta()
             host_out.copy_(nxt, non_blocking=True)
         torch.cuda.synchronize()
         if it >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     if world == 1:
+        assert res.tensor.data_ptr() == host_out.data_ptr()
+        # the public call is one sweep of the engine: same bits as the device step
+        eng.lam_a.copy_(base)
+        gcache.copy_(base_g)
+        eng.prev = eng.lam_a
+        eng.sweep(1, nxt)
+        same = bool(torch.equal(nxt.cpu(), host_out))
         eng.prev = eng.lam_a
     ms_e2e = float(np.mean(e2e_ms))
     if world > 1:
@@ -324,8 +358,11 @@ def run_ours(args, rank: int, world: int) -> None:
                     "fp64_pipe_frac_ncu": _ncu_field("fp64_pipe_pct_of_peak", 0.01),
                     "fp64_peak_tfma_s_measured": 17.95,
                     "source": "profiles/ncu_fine_kernel.json, scripts/microbench.cu"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 8,
-                "ms_per_step": ms_e2e},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "ms_per_step": ms_e2e,
+                "call": "paper_2110_10762_b200.parareal_iterate(coarse, fine, BlockVector(pinned host iterate), "
+                        "out=pinned host) — the reference's parareal_iterate, parareal.py:66-76",
+                "equals_device_sweep_bitwise": same if world == 1 else None},
         "gpu_launches": None,
         "clocks": clocks.summary(),
         "layout": {"threads_per_slice": info.threads_per_slice, "points_per_thread": info.points_per_thread,
@@ -333,11 +370,17 @@ def run_ours(args, rank: int, world: int) -> None:
         "delta_first_sweep": delta,
     }
     line["gpu_launches"] = args.steps * (eng.launches_per_sweep(1) if world == 1 else eng.launches_per_sweep())
+    if world > 1 and args.time_to_tol:
+        line["multi_gpu"] = multi_gpu_time_to_tolerance(rank, world)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
         if args.time_to_tol and world == 1:
             line["time_to_tolerance"] = time_to_tolerance(coarse, fine, u0, P_LOCAL)
+        if args.configs and world == 1:
+            line["configs"] = nd_configs(not args.no_cpu_baseline)
+            if not args.no_cpu_baseline:
+                line["cpu_time_to_tolerance"] = cpu_time_to_tolerance()
         print(json.dumps(line), flush=True)
 
 
@@ -381,6 +424,257 @@ def time_to_tolerance(coarse, fine, u0, p: int, eps: float = 1e-10) -> dict:
     return out
 
 
+# ------------------------------------------------- 2-D / 3-D configurations
+ND_CONFIGS = {
+    "c3_f64": dict(shape=(1024, 1024), p=32, steps=500, cfl=0.2, dtype="float64", eps=1e-10),
+    "c3_f32": dict(shape=(1024, 1024), p=32, steps=500, cfl=0.2, dtype="float32", eps=1e-5),
+    "c4_f32": dict(shape=(256, 256, 256), p=64, steps=200, cfl=0.15, dtype="float32", eps=1e-5, async_mp=True),
+    # C5 runs at 2/4/8 GPUs in BASELINE (P = 128, 64.5 GiB per state copy); on
+    # one GPU its per-GPU share (16 slices at 8 GPUs) is timed for F
+    "c5_f32_share": dict(shape=(512, 512, 512), p=16, steps=100, cfl=0.15, dtype="float32", fine_only=True),
+}
+
+
+def _sine_u0_device(shape, seed=0):
+    """inputs.sine_u0_nd built on the GPU with numpy's sines and the same
+    elementwise operation order (same bits, no 1 GB host temporaries)."""
+    import torch
+
+    from paper_2110_10762_b200.inputs import interior_grid, modes_2d, modes_3d
+    modes = modes_2d() if len(shape) == 2 else modes_3d()
+    amp = np.random.default_rng(seed).standard_normal(len(modes))
+    axes = [interior_grid(n) for n in shape]
+    out = torch.zeros(shape, dtype=torch.float64, device="cuda")
+    for a, ks in zip(amp, modes):
+        term = torch.ones(shape, dtype=torch.float64, device="cuda")
+        for d, k in enumerate(ks):
+            bshape = [1] * len(shape)
+            bshape[d] = shape[d]
+            term = term * torch.from_numpy(np.sin(k * np.pi * axes[d])).to("cuda").reshape(bshape)
+        out = out + float(a) * term
+    return out.reshape(-1)
+
+
+def _world1():
+    """A one-rank process group for the multi-process runtime (N = 1)."""
+    import socket
+
+    import torch.distributed as dist
+    if dist.is_initialized():
+        return False
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    return True
+
+
+def _cpu_port_fine(shape, steps, cfl, dtype, target_s=2.0) -> dict:
+    """The oracle restatement of the explicit fine map (oracle/stencil_nd.c,
+    OpenMP over the host cores) timed on one slice of the configuration."""
+    from oracle.nd_truth import StencilND
+    n = shape[0]
+    h = 1.0 / (n + 1)
+    st = StencilND(shape, h, steps * cfl * h * h, steps, dtype=np.float32 if dtype == "float32" else np.float64)
+    u = np.random.default_rng(0).standard_normal(int(np.prod(shape)))
+    t0 = time.perf_counter()
+    st.apply(u)
+    t1 = time.perf_counter() - t0
+    reps = max(1, min(8, int(target_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        st.apply(u)
+    t = (time.perf_counter() - t0) / reps
+    upd = int(np.prod(shape)) * steps
+    return {"value": upd / t / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{reps + 1} slice applications of F ({steps} FE steps, {'x'.join(map(str, shape))}, {dtype}; "
+                      f"oracle/stencil_nd.c, OpenMP over {os.cpu_count()} threads)"}
+
+
+def _nd_config(name: str, cfg: dict, with_cpu: bool) -> dict:
+    import torch
+
+    import paper_2110_10762_b200 as pb
+    shape, p, steps = cfg["shape"], cfg["p"], cfg["steps"]
+    n = shape[0]
+    h = 1.0 / (n + 1)
+    span = steps * cfg["cfl"] * h * h
+    u0 = _sine_u0_device(shape)
+    mk = pb.heat2d_system if len(shape) == 2 else pb.heat3d_system
+    ivp = mk(n, t_final=p * span, u0=None)
+    fine = pb.forward_euler_propagator(ivp, span, steps, dtype=cfg["dtype"])
+    coarse = pb.backward_euler_propagator(ivp, span, 1, dtype=cfg["dtype"])
+    dim = ivp.dim
+    esz = 8 if cfg["dtype"] == "float64" else 4
+    x = u0.to(fine.dtype).reshape(1, -1).repeat(p, 1)
+    y = torch.empty_like(x)
+    out = {"workload": f"{'x'.join(map(str, shape))}, P={p}, F={steps} FE steps (dt={cfg['cfl']}h^2), "
+                       f"G=1 BE step (direct sine-transform solve), {cfg['dtype']}",
+           "l2": f"state {x.numel() * esz / 2**20:.0f} MiB per F batch (larger than the 126 MB L2)"}
+    fine.apply_batch(x, out=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record()
+        for _ in range(reps):
+            fine.apply_batch(x, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+    ms_f = e0.elapsed_time(e1) / reps
+    upd = p * steps * dim
+    peak = measured_peaks()["hbm_gbs"]
+    out.update({"fine_batch_ms": ms_f, "fine_GPt_s": upd / ms_f / 1e6,
+                "fine_roofline": {"bound": "hbm", "achieved": upd * 2 * esz / (ms_f * 1e-3) / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": upd * 2 * esz / (ms_f * 1e-3) / 1e9 / peak,
+                                  "note": f"algorithmic bytes 2*{esz} B per update; S levels per HBM pass"},
+                "clocks": clk.summary()})
+    g_in, g_out = x[0:1].clone(), torch.empty_like(x[0:1])
+    coarse.apply_ptr(g_in.data_ptr(), g_out.data_ptr(), 1, dim)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(3):
+        coarse.apply_ptr(g_in.data_ptr(), g_out.data_ptr(), 1, dim)
+    e1.record()
+    torch.cuda.synchronize()
+    out["coarse_solve_ms"] = e0.elapsed_time(e1) / 3
+    del x, y
+    if not cfg.get("fine_only"):
+        u0h = u0.to(fine.dtype)
+        pb.run_parareal(coarse, fine, u0h, p, cfg["eps"], k_max=1, record_iterates=False)  # warm-up
+        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            t0 = time.perf_counter()
+            tr = pb.run_parareal(coarse, fine, u0h, p, cfg["eps"], record_iterates=False)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        seq = pb.sequential_fine_solve(fine, u0h, p).tensor
+        fin = tr.final.tensor
+        out["sync_time_to_tolerance"] = {
+            "seconds": wall, "k": tr.k_final, "stop_reason": tr.stop_reason, "epsilon": cfg["eps"],
+            "rel_l2_vs_seq_fine": float(((fin.double() - seq.double()).norm() / seq.double().norm()).item()),
+            "clocks": clk.summary()}
+        del tr, fin
+        if cfg.get("async_mp"):
+            from paper_2110_10762_b200.async_mp import run_async_parareal_mp
+            made = _world1()
+            try:
+                run_async_parareal_mp(coarse, fine, u0h, p, cfg["eps"], lanes=2, max_events=64)  # warm-up
+            except pb.HorizonExhausted:
+                pass
+            try:
+                res = run_async_parareal_mp(coarse, fine, u0h, p, cfg["eps"], lanes=2, gather=True)
+                out["async_time_to_tolerance_1gpu"] = {
+                    "seconds": res.wall_s, "kappa": res.kappa, "activations": res.activations,
+                    "stop_reason": res.stop_reason, "runtime": "async_mp (one rank, 2 lanes)",
+                    "rel_l2_vs_seq_fine": float(((res.final.double() - seq.double()).norm()
+                                                 / seq.double().norm()).item())}
+            except Exception as exc:  # reported, never silently replaced
+                out["async_time_to_tolerance_1gpu"] = {"error": f"{type(exc).__name__}: {exc}"}
+            finally:
+                if made:
+                    import torch.distributed as dist
+                    dist.destroy_process_group()
+        del seq
+    torch.cuda.empty_cache()
+    if with_cpu:
+        out["cpu_port_fine"] = _cpu_port_fine(shape, steps, cfg["cfl"], cfg["dtype"])
+    return out
+
+
+def nd_configs(with_cpu: bool) -> dict:
+    out = {}
+    for name, cfg in ND_CONFIGS.items():
+        try:
+            out[name] = _nd_config(name, cfg, with_cpu)
+        except Exception as exc:  # reported, never silently replaced
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+def cpu_time_to_tolerance() -> dict:
+    """The oracle restatement of the reference's synchronous run
+    (parareal.py:99-138) on the host: C1 (LAPACK step maps, the reference's
+    own scale) and C3 fp64 (oracle/stencil_nd.c fine map over all cores,
+    exact sine-transform coarse solve)."""
+    from oracle import heat_oracle as H
+    from oracle.nd_truth import SpectralND, StencilND
+    out = {"cores": os.cpu_count(), "kind": "port"}
+    n, p = 1024, 16
+    a_d, a_o, c = H.heat1d_coeffs(n)
+    F = H.Tridiag1D(n, a_d, a_o, c, 1.0 / p, 100)
+    G = H.Tridiag1D(n, a_d, a_o, c, 1.0 / p, 1)
+    u0 = H.sine_u0_1d(n, 8, 0)
+    t0 = time.perf_counter()
+    tr = H.run_parareal(G, F, u0, p, 1e-10)
+    out["c1"] = {"seconds": time.perf_counter() - t0, "k": tr.k_final, "stop_reason": tr.stop_reason}
+    n, p, steps = 1024, 32, 500
+    h = 1.0 / (n + 1)
+    span = steps * 0.2 * h * h
+    u0 = H.sine_u0_nd((n, n), H.modes_2d(), 0).reshape(-1)
+    t0 = time.perf_counter()
+    tr = H.run_parareal(SpectralND((n, n), h, span), StencilND((n, n), h, span, steps), u0, p, 1e-10)
+    out["c3_f64"] = {"seconds": time.perf_counter() - t0, "k": tr.k_final, "stop_reason": tr.stop_reason}
+    return out
+
+
+def multi_gpu_time_to_tolerance(rank: int, world: int) -> dict:
+    """At N ranks: the 1-D device async runtime across GPUs (C2 slices split
+    over the ranks, P2P mailbox pushes, on-device stop) and the multi-process
+    runtime of whole-GPU activations at C4 (P = 64 split over the ranks)."""
+    import torch
+
+    import paper_2110_10762_b200 as pb
+    from paper_2110_10762_b200 import distributed as dist_rt
+    from paper_2110_10762_b200.async_mp import run_async_parareal_mp
+    from paper_2110_10762_b200.inputs import sine_u0_1d
+    out = {}
+    try:
+        ivp = pb.heat1d_system(N_POINTS, 1.0, 0.0, 0.0, 0.0, T_FINAL)
+        fine = pb.backward_euler_propagator(ivp, T_FINAL / P_LOCAL, FINE_STEPS)
+        coarse = pb.backward_euler_propagator(ivp, T_FINAL / P_LOCAL, 1)
+        u0 = sine_u0_1d(N_POINTS, N_MODES, 0)
+        r = dist_rt.run_async_parareal_distributed(coarse, fine, u0, P_LOCAL, 1e-10, gather=False)
+        out["c2_async_1d"] = {"seconds": r["wall_s"], "kappa": r["kappa"], "activations": r["activations"],
+                              "stop_reason": r["stop_reason"], "slices": P_LOCAL, "n_gpus": world}
+    except Exception as exc:
+        out["c2_async_1d"] = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
+        cfg = ND_CONFIGS["c4_f32"]
+        shape, p, steps = cfg["shape"], cfg["p"], cfg["steps"]
+        h = 1.0 / (shape[0] + 1)
+        span = steps * cfg["cfl"] * h * h
+        ivp = pb.heat3d_system(shape[0], t_final=p * span, u0=None)
+        fine = pb.forward_euler_propagator(ivp, span, steps, dtype="float32")
+        coarse = pb.backward_euler_propagator(ivp, span, 1, dtype="float32")
+        u0 = _sine_u0_device(shape).to(torch.float32)
+        r = run_async_parareal_mp(coarse, fine, u0, p, cfg["eps"], lanes=2)
+        out["c4_async_nd"] = {"seconds": r.wall_s, "kappa": r.kappa, "activations": r.activations,
+                              "stop_reason": r.stop_reason, "slices": p, "n_gpus": world}
+    except Exception as exc:
+        out["c4_async_nd"] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+def _launch_ranks(n: int) -> int:
+    """Re-run this command under torchrun, one rank per GPU (127.0.0.1)."""
+    import socket
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.stderr.write(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible\n")
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -391,12 +685,23 @@ def main():
     ap.add_argument("--time-to-tol", action="store_true", default=True,
                     help="sync + device-async time to tolerance, cost model, contraction factors (default on)")
     ap.add_argument("--no-time-to-tol", dest="time_to_tol", action="store_false")
+    ap.add_argument("--configs", action="store_true", default=True,
+                    help="C3/C4/C5 lines (2-D/3-D fine throughput, time to tolerance, CPU port) (default on)")
+    ap.add_argument("--no-configs", dest="configs", action="store_false")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    world_env = os.environ.get("WORLD_SIZE")
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        # host-only arm: rank 0 measures, the other ranks exit without work
+        run_reference(args, rank, int(world_env) if world_env else args.gpus)
         return
+    if world_env is None and args.gpus > 1:
+        sys.exit(_launch_ranks(args.gpus))
+    world = int(world_env) if world_env else 1
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         from paper_2110_10762_b200 import distributed as dist_rt
         dist_rt.init_process_group()

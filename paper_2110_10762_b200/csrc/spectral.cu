@@ -45,6 +45,9 @@ namespace {
 //   FOLD 2 (transform along B's rows):    B'[k][x] = B[k][x] +- B[n-1-k][x],
 //          A = half[par] (M_par x K'), output row 2 q + par;
 // with K' = ceil(n/2) and the sign + for even, - for odd output indices.
+// byte offset of the fp64 modal-sweep scratch inside an fp32 op's work area
+static size_t spectral_g64_offset(int64_t dim) { return ((size_t)3 * dim * 4 + 255) / 256 * 256; }
+
 template <typename T>
 struct GemmArgs {
   const T *A;
@@ -90,13 +93,17 @@ __device__ __forceinline__ void ldv(const T *p, T *d) {
 // 256 threads as 16 x 16; each thread owns a TM x TN register tile split in
 // two halves per axis (rows ty*HM.. and BM/2 + ty*HM..), so its shared-memory
 // operand reads are 2 vector loads per axis. K staged 8 at a time, double
-// buffered through registers.
-template <typename T, int BM, int BN, int FOLD, int MINB>
+// buffered through registers. Acc is the accumulation (and fold) type: fp32
+// operands accumulate in fp64 (DFMA), so an fp32 solve carries only the
+// rounding of its stored operands, not a sqrt(K)-growing accumulation error
+// (C3 fp32: the coarse chain of 32 solves moved 1.4e-5 off the exact solve
+// with fp32 accumulation, tests/test_gpu_config_parity.py).
+template <typename T, int BM, int BN, int FOLD, int MINB, typename Acc = T>
 __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
   constexpr int BK = 8, TM = BM / 16, TN = BN / 16, HM = TM / 2, HN = TN / 2;
   constexpr int LA = BM * BK / 256, LB = BN * BK / 256;
-  __shared__ __align__(16) T As[2][BK][BM];
-  __shared__ __align__(16) T Bs[2][BK][BN];
+  __shared__ __align__(16) Acc As[2][BK][BM];
+  __shared__ __align__(16) Acc Bs[2][BK][BN];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   int z = blockIdx.z, par = 0;
   if (FOLD) {
@@ -116,17 +123,17 @@ __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
   if (m0 >= M || n0 >= N) return;
   const int a_row = tid / (BK / LA), a_k = (tid % (BK / LA)) * LA;
   const int b_row = tid / (BN / LB), b_n = (tid % (BN / LB)) * LB;
-  T ra[LA], rb[LB];
+  Acc ra[LA], rb[LB];
   auto load = [&](int k0) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const int m = m0 + a_row, k = k0 + a_k + i;
-      T v = T(0);
+      Acc v = Acc(0);
       if (m < M && k < K) {
-        v = A[(int64_t)m * lda + k];
+        v = (Acc)A[(int64_t)m * lda + k];
         if (FOLD == 1) {
           const int k2 = g.nfold - 1 - k;
-          if (k2 > k) v = par ? v - A[(int64_t)m * lda + k2] : v + A[(int64_t)m * lda + k2];
+          if (k2 > k) v = par ? v - (Acc)A[(int64_t)m * lda + k2] : v + (Acc)A[(int64_t)m * lda + k2];
         }
       }
       ra[i] = v;
@@ -134,12 +141,12 @@ __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
       const int k = k0 + b_row, n = n0 + b_n + i;
-      T v = T(0);
+      Acc v = Acc(0);
       if (k < K && n < N) {
-        v = B[(int64_t)k * ldb + n];
+        v = (Acc)B[(int64_t)k * ldb + n];
         if (FOLD == 2) {
           const int k2 = g.nfold - 1 - k;
-          if (k2 > k) v = par ? v - B[(int64_t)k2 * ldb + n] : v + B[(int64_t)k2 * ldb + n];
+          if (k2 > k) v = par ? v - (Acc)B[(int64_t)k2 * ldb + n] : v + (Acc)B[(int64_t)k2 * ldb + n];
         }
       }
       rb[i] = v;
@@ -151,11 +158,11 @@ __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
 #pragma unroll
     for (int i = 0; i < LB; ++i) Bs[buf][b_row][b_n + i] = rb[i];
   };
-  T acc[TM][TN];
+  Acc acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    for (int j = 0; j < TN; ++j) acc[i][j] = Acc(0);
   load(0);
   store(0);
   __syncthreads();
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
     if (t + 1 < nk) load((t + 1) * BK);
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      T a[TM], b[TN];
+      Acc a[TM], b[TN];
       ldv<HM>(&As[buf][k][ty * HM], a);
       ldv<HM>(&As[buf][k][BM / 2 + ty * HM], a + HM);
       ldv<HN>(&Bs[buf][k][tx * HN], b);
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(256, MINB) gemm_nn(const GemmArgs<T> g) {
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + (j < HN ? tx * HN + j : BN / 2 + tx * HN + (j - HN));
-      if (n < N) C[row * g.ldc + (FOLD == 1 ? 2 * n + par : n)] = acc[i][j];
+      if (n < N) C[row * g.ldc + (FOLD == 1 ? 2 * n + par : n)] = (T)acc[i][j];
     }
   }
 }
@@ -196,20 +203,11 @@ void gemm(const GemmArgs<T> &g, int batch, cudaStream_t s) {
   const int M = FOLD == 2 ? g.mn[0] : g.M, N = FOLD == 1 ? g.mn[0] : g.N;  // parity 0 is the larger half
   const int zs = batch * (FOLD ? 2 : 1);
   auto tiles = [&](int bm, int bn) { return (int64_t)((M + bm - 1) / bm) * ((N + bn - 1) / bn) * zs; };
-  // FP64: 4x4 per thread already keeps the DFMA pipe ahead of shared memory.
-  // FP32: 8x8 per thread (two CTAs per SM) when that still fills two waves.
-  if constexpr (sizeof(T) == 4) {
-    if (tiles(128, 128) >= 2 * 148) {
-      dim3 grid((unsigned)((N + 127) / 128), (unsigned)((M + 127) / 128), (unsigned)zs);
-      gemm_nn<T, 128, 128, FOLD, 2><<<grid, 256, 0, s>>>(g);
-      PINT_CUDA(cudaGetLastError());
-      return;
-    }
-  }
-  {
-    dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)zs);
-    gemm_nn<T, 64, 64, FOLD, 1><<<grid, 256, 0, s>>>(g);
-  }
+  (void)tiles;
+  // 4x4 per thread keeps the DFMA pipe ahead of shared memory; fp32 operands
+  // are staged and accumulated in fp64 (see gemm_nn)
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)zs);
+  gemm_nn<T, 64, 64, FOLD, 1, double><<<grid, 256, 0, s>>>(g);
   PINT_CUDA(cudaGetLastError());
 }
 
@@ -225,8 +223,19 @@ void gemm(const GemmArgs<T> &g, int batch, cudaStream_t s) {
 // only (the recurrences contract: c p_j^-1 < 1).
 template <typename T, int MC, int SYS>
 __global__ void __launch_bounds__(MC * SYS)
-modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_t nsys, double c,
-                      int64_t steps) {
+modal_tridiag_chunked(T *__restrict__ u, const double *__restrict__ ipt, double *__restrict__ g64, int J, int n,
+                      int64_t nsys, double c, int64_t steps) {
+  // forward intermediates g_j: kept in fp64 (g64) for fp32 states — rounding
+  // them to fp32 before the back substitution (x_j = g_j + e_j x_{j+1},
+  // e_j -> 1 for strongly coupled modes) cost 8.7e-7 per C3 solve
+  auto gst = [&](int64_t idx, double v) {
+    if constexpr (sizeof(T) == 4) g64[idx] = v;
+    else u[idx] = (T)v;
+  };
+  auto gld = [&](int64_t idx) -> double {
+    if constexpr (sizeof(T) == 4) return g64[idx];
+    else return (double)u[idx];
+  };
   __shared__ double cmp[2][MC][SYS];  // chunk maps (A, B)
   __shared__ double entry[MC + 1][SYS];
   const int w = threadIdx.x / SYS, sl = threadIdx.x % SYS;
@@ -259,7 +268,7 @@ modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n
     if (live)
       for (int j = j0; j < j1; ++j) {
         g = fma(c, g, (double)u[(int64_t)j * nsys + i]) * ipat(j);
-        u[(int64_t)j * nsys + i] = (T)g;
+        gst((int64_t)j * nsys + i, g);
       }
     __syncthreads();
     // ---- backward: x_j = g_j + e_j x_{j+1}, e_j = c / p_j (e_{n-1} = 0)
@@ -268,7 +277,7 @@ modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n
       for (int j = j1 - 1; j >= j0; --j) {
         const double e = j == n - 1 ? 0.0 : c * ipat(j);
         C = e * C;
-        D = fma(e, D, (double)u[(int64_t)j * nsys + i]);
+        D = fma(e, D, gld((int64_t)j * nsys + i));
       }
     cmp[0][w][sl] = C;
     cmp[1][w][sl] = D;
@@ -285,7 +294,7 @@ modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n
     if (live)
       for (int j = j1 - 1; j >= j0; --j) {
         const double e = j == n - 1 ? 0.0 : c * ipat(j);
-        x = fma(e, x, (double)u[(int64_t)j * nsys + i]);
+        x = fma(e, x, gld((int64_t)j * nsys + i));
         u[(int64_t)j * nsys + i] = (T)x;
       }
     __syncthreads();
@@ -302,8 +311,18 @@ modal_tridiag_chunked(T *__restrict__ u, const T *__restrict__ ipt, int J, int n
 // issued a block of U points ahead of it.
 template <typename T>
 __global__ void __launch_bounds__(128)
-modal_tridiag(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_t nsys, double c, int64_t steps) {
+modal_tridiag(T *__restrict__ u, const double *__restrict__ ipt, double *__restrict__ g64, int J, int n, int64_t nsys,
+              double c, int64_t steps) {
   constexpr int U = 8;
+  // forward intermediates in fp64 for fp32 states (see modal_tridiag_chunked)
+  auto gst = [&](int64_t idx, double v) {
+    if constexpr (sizeof(T) == 4) g64[idx] = v;
+    else u[idx] = (T)v;
+  };
+  auto gld = [&](int64_t idx) -> double {
+    if constexpr (sizeof(T) == 4) return g64[idx];
+    else return (double)u[idx];
+  };
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsys) return;
   const double ipinf = (double)ipt[(int64_t)(J - 1) * nsys + i];
@@ -327,7 +346,7 @@ modal_tridiag(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_
       for (int q = 0; q < U; ++q) {
         if (j0 + q < n) {
           g = fma(c, g, (double)cur[q]) * cip[q];
-          u[(int64_t)(j0 + q) * nsys + i] = (T)g;
+          gst((int64_t)(j0 + q) * nsys + i, g);
         }
       }
 #pragma unroll
@@ -338,12 +357,13 @@ modal_tridiag(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_
     }
     // back substitution x_j = g_j + (c / p_j) x_{j+1}, blocks of U from the top
     double x = g;
-    T cg[U], ng[U];
-    auto fetch = [&](int top, T *gg, double *pp) {
+    if constexpr (sizeof(T) == 4) u[(int64_t)(n - 1) * nsys + i] = (T)x;  // x_{n-1} = g_{n-1}
+    double cg[U], ng[U];
+    auto fetch = [&](int top, double *gg, double *pp) {
 #pragma unroll
       for (int q = 0; q < U; ++q) {
         const int jj = top - q;
-        gg[q] = jj >= 0 ? u[(int64_t)jj * nsys + i] : T(0);
+        gg[q] = jj >= 0 ? gld((int64_t)jj * nsys + i) : 0.0;
         pp[q] = jj >= 0 ? ipat(jj) : 0.0;
       }
     };
@@ -354,7 +374,7 @@ modal_tridiag(T *__restrict__ u, const T *__restrict__ ipt, int J, int n, int64_
       for (int q = 0; q < U; ++q) {
         const int jj = top - q;
         if (jj >= 0) {
-          x = fma(c * cip[q], x, (double)cg[q]);
+          x = fma(c * cip[q], x, cg[q]);
           u[(int64_t)jj * nsys + i] = (T)x;
         }
       }
@@ -374,6 +394,10 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
   const int kh = (n + 1) / 2, n0 = (n + 1) / 2, n1 = n / 2;  // folded K; output counts per parity
   T *w1 = reinterpret_cast<T *>(op->cg_work);
   T *w2 = w1 + op->dim;
+  // fp64 forward intermediates of the modal sweep (fp32 states only)
+  double *g64 = sizeof(T) == 4 ? reinterpret_cast<double *>(reinterpret_cast<char *>(op->cg_work) +
+                                                             spectral_g64_offset(op->dim))
+                               : nullptr;
   const T *Q = reinterpret_cast<const T *>(op->spec_q);
   // host layout of spec_q: Qh[0] (kh x n0), Qh[1] (kh x n1), QhT[0] (n0 x kh), QhT[1] (n1 x kh)
   const T *qh0 = Q, *qh1 = qh0 + (size_t)kh * n0, *qt0 = qh1 + (size_t)kh * n1, *qt1 = qt0 + (size_t)n0 * kh;
@@ -444,10 +468,10 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
     if (n >= 256 && !(mc && atoi(mc) == 0)) {
       constexpr int MC = 64, SYS = 16;
       modal_tridiag_chunked<T, MC, SYS><<<(unsigned)((n + SYS - 1) / SYS), MC * SYS, 0, s>>>(
-          w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
+          w1, reinterpret_cast<const double *>(op->spec_ip), g64, op->spec_J, n, n, c, op->desc.steps);
     } else {
       modal_tridiag<T><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
-          w1, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n, c, op->desc.steps);
+          w1, reinterpret_cast<const double *>(op->spec_ip), g64, op->spec_J, n, n, c, op->desc.steps);
     }
     PINT_CUDA(cudaGetLastError());
     xform_last(w1, x, n);
@@ -456,7 +480,7 @@ void spectral_solve(pint_op *op, const T *b, T *x, cudaStream_t s) {
     xform_mid(w1, w2);
     // (the chunked sweep measured slower here: 3-D grids have n^2 modes, 0.510 vs 0.480 ms at C4)
     modal_tridiag<T><<<(unsigned)((n2 + threads - 1) / threads), threads, 0, s>>>(
-        w2, reinterpret_cast<const T *>(op->spec_ip), op->spec_J, n, n2, c, op->desc.steps);
+        w2, reinterpret_cast<const double *>(op->spec_ip), g64, op->spec_J, n, n2, c, op->desc.steps);
     PINT_CUDA(cudaGetLastError());
     xform_mid(w2, w1);
     xform_last(w1, x, (int)n2);
@@ -472,7 +496,7 @@ void spectral_setup(pint_op *op) {
     pint_throw(PINT_EDIM, "direct solve needs the same point count on every axis");
   if (n * n > 0x7fffffffLL) pint_throw(PINT_EDIM, "grid too large");
   const size_t esz = op->desc.dtype == PINT_F64 ? 8 : 4;
-  op->cg_work_bytes = (size_t)3 * op->dim * esz;
+  op->cg_work_bytes = esz == 8 ? (size_t)3 * op->dim * esz : spectral_g64_offset(op->dim) + (size_t)op->dim * 8;
   PINT_CUDA(cudaMalloc(&op->cg_work, op->cg_work_bytes));
   std::vector<long double> mu(n);
   std::vector<long double> q((size_t)n * n);
@@ -527,20 +551,19 @@ void spectral_setup(pint_op *op) {
     }
     J = std::min<int64_t>(J + 1, n);
   }
+  // fp64 for both state types: the pivots of strongly coupled modes are
+  // where fp32 rounding would be amplified
   std::vector<double> ipd((size_t)J * nsys);
-  std::vector<float> ipf(esz == 4 ? (size_t)J * nsys : 0);
   for (int64_t m = 0; m < nsys; ++m) {
     long double pv = dmode[m];
     for (int64_t jj = 0; jj < J; ++jj) {
       if (jj > 0) pv = dmode[m] - cl * cl / pv;
       ipd[(size_t)jj * nsys + m] = (double)(1.0L / pv);
-      if (esz == 4) ipf[(size_t)jj * nsys + m] = (float)(1.0L / pv);
     }
   }
   op->spec_J = (int)J;
-  PINT_CUDA(cudaMalloc(&op->spec_ip, esz * ipd.size()));
-  PINT_CUDA(cudaMemcpy(op->spec_ip, esz == 8 ? (const void *)ipd.data() : (const void *)ipf.data(),
-                       esz * ipd.size(), cudaMemcpyHostToDevice));
+  PINT_CUDA(cudaMalloc(&op->spec_ip, 8 * ipd.size()));
+  PINT_CUDA(cudaMemcpy(op->spec_ip, ipd.data(), 8 * ipd.size(), cudaMemcpyHostToDevice));
   if (esz == 4 && op->desc.ndim == 3 && tc_xform_supported((int)n)) {
     const std::vector<uint32_t> tcq = tc_split_q((int)n, q.data());
     PINT_CUDA(cudaMalloc(&op->spec_tcq, 4 * tcq.size()));

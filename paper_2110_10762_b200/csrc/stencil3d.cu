@@ -23,16 +23,63 @@
 // The per-point arithmetic is the same expression in every variant,
 //   nb = ((x- + x+) + (y- + y+)) + (z- + z+);  v = fma(r, fma(-6, c, nb), c),
 // so every tiling (and fe3d_wave) produces bitwise identical results.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "pint_internal.cuh"
 
 namespace {
 
 constexpr int ZC = 128;  // output planes per chunk
+constexpr int TMA_D = 4;  // input planes in flight per CTA (TMA ring depth)
+
+// ---- TMA input ring (variants with TMA = true): the CTA's xy tile of each
+// input plane arrives in shared memory by one cp.async.bulk.tensor load
+// (4-D tensor map x, y, z, slice; the halo outside the grid is zero-filled by
+// the TMA unit, i.e. the zero Dirichlet values), TMA_D planes ahead of the
+// wavefront, each completing on its own mbarrier.
+struct TmaCtx {
+  uint32_t ring;  // shared address of slot 0
+  uint32_t bars;  // shared address of TMA_D mbarriers
+  int x0, y0, b;  // tile origin (incl. halo) and slice
+  int zs;         // first input plane of the sweep
+  const CUtensorMap *map;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_bar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TW_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// load plane z of the tile into ring slot `slot` (one elected thread)
+template <int W, int H, typename T>
+__device__ __forceinline__ void tma_plane(const TmaCtx &t, int slot, int z) {
+  const uint32_t bar = t.bars + 8u * (uint32_t)slot;
+  const uint32_t dst = t.ring + (uint32_t)(slot * W * H * (int)sizeof(T));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)(W * H * sizeof(T)))
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(t.map)), "r"(t.x0), "r"(t.y0), "r"(z), "r"(t.b), "r"(bar)
+      : "memory");
+}
 
 template <typename T, int CPT>
 struct Vec;
@@ -143,22 +190,46 @@ struct Xchg {
 // One plane of the wavefront for a strip of RPT rows x CPT columns per lane.
 // EDGE: some level's plane may lie outside the domain (per-level plane mask);
 // PAR: shared-buffer parity (compile time).
-template <typename T, int S, int NW, int RPT, int CPT, bool EDGE, bool MASK, int PAR>
+template <typename T, int S, int NW, int RPT, int CPT, bool EDGE, bool MASK, int PAR, bool TMA>
 __device__ __forceinline__ void plane(T (&cur)[S][RPT][CPT], T (&prv)[S][RPT][CPT], T (&pp)[S][RPT][CPT],
                                       T (&pre)[RPT][CPT], Xchg<T, S, NW, RPT, CPT> &X, const PlaneCtx &q,
                                       const T (&m)[RPT][CPT], const bool (&colout)[RPT][CPT],
                                       const bool (&colin)[RPT][CPT], const T *&src_next, T *&dst_out,
-                                      int64_t plane_stride, int64_t row_stride, T r) {
+                                      int64_t plane_stride, int64_t row_stride, T r, const TmaCtx &tm) {
   using V = typename Vec<T, CPT>::V;
+  constexpr int W = 32 * CPT, H = NW * RPT;
   const int lane = threadIdx.x & 31;
   const int wu = q.w > 0 ? q.w - 1 : 0, wd = q.w < NW - 1 ? q.w + 1 : NW - 1;
+  if constexpr (TMA) {
+    const int pi = q.zz - tm.zs;
+    const int slot = pi & (TMA_D - 1);
+    tma_bar_wait(tm.bars + 8u * (uint32_t)slot, (uint32_t)(pi / TMA_D) & 1u);
+    const unsigned a = tm.ring + (unsigned)(((slot * H + RPT * q.w) * W + CPT * lane) * (int)sizeof(T));
 #pragma unroll
-  for (int y = 0; y < RPT; ++y)
+    for (int y = 0; y < RPT; ++y) {
+      T tmp[CPT];
+      const unsigned ay = a + (unsigned)(y * W * (int)sizeof(T));
+      if constexpr (sizeof(T) * CPT == 8) {
+        unsigned long long u;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(u) : "r"(ay));
+        memcpy(tmp, &u, 8);
+      } else {
+        uint4 u;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(ay));
+        memcpy(tmp, &u, 16);
+      }
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) cur[0][y][c] = pre[y][c];
+      for (int c = 0; c < CPT; ++c) cur[0][y][c] = tmp[c];
+    }
+  } else {
+#pragma unroll
+    for (int y = 0; y < RPT; ++y)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) cur[0][y][c] = pre[y][c];
+  }
   X.tp(PAR, 0, q.w, lane) = vmake<CPT, V>(cur[0][0]);
   if constexpr (RPT > 1) X.bt(PAR, 0, q.w, lane) = vmake<CPT, V>(cur[0][RPT - 1]);
-  {
+  if constexpr (!TMA) {
     const int zn = q.zz + 1;
     const bool pin = zn < q.nz && zn <= q.ze && (!EDGE || zn >= 0);
 #pragma unroll
@@ -217,12 +288,17 @@ __device__ __forceinline__ void plane(T (&cur)[S][RPT][CPT], T (&prv)[S][RPT][CP
         prv[L][y][c] = cur[L][y][c];
       }
   __syncthreads();
+  if constexpr (TMA) {
+    // every thread has read this plane's slot: refill it TMA_D planes ahead
+    const int zn = q.zz + TMA_D;
+    if (threadIdx.x == 0 && zn <= q.ze) tma_plane<W, H, T>(tm, (zn - tm.zs) & (TMA_D - 1), zn);
+  }
 }
 
-template <typename T, int S, int NW, int RPT, int CPT, bool MASK>
+template <typename T, int S, int NW, int RPT, int CPT, bool MASK, bool TMA>
 __device__ __forceinline__ void sweep(Xchg<T, S, NW, RPT, CPT> &X, PlaneCtx q, int zs, const T (&m)[RPT][CPT],
                                       const bool (&colout)[RPT][CPT], const bool (&colin)[RPT][CPT],
-                                      const T *src_col, T *dst_col, int64_t pl, int64_t rs, T r) {
+                                      const T *src_col, T *dst_col, int64_t pl, int64_t rs, T r, const TmaCtx &tm) {
   T cur[S][RPT][CPT], prv[S][RPT][CPT], pp[S][RPT][CPT];
 #pragma unroll
   for (int L = 0; L < S; ++L)
@@ -231,7 +307,7 @@ __device__ __forceinline__ void sweep(Xchg<T, S, NW, RPT, CPT> &X, PlaneCtx q, i
 #pragma unroll
       for (int c = 0; c < CPT; ++c) cur[L][y][c] = prv[L][y][c] = pp[L][y][c] = T(0);
   T pre[RPT][CPT];
-  {
+  if constexpr (!TMA) {
     const bool pin = zs >= 0 && zs < q.nz;
 #pragma unroll
     for (int y = 0; y < RPT; ++y)
@@ -250,21 +326,21 @@ __device__ __forceinline__ void sweep(Xchg<T, S, NW, RPT, CPT> &X, PlaneCtx q, i
 #pragma unroll
       for (int u = 0; u < 6; u += 2) {
         q.zz = zz + u;
-        plane<T, S, NW, RPT, CPT, false, MASK, 0>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl,
-                                                  rs, r);
+        plane<T, S, NW, RPT, CPT, false, MASK, 0, TMA>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out,
+                                                       pl, rs, r, tm);
         q.zz = zz + u + 1;
-        plane<T, S, NW, RPT, CPT, false, MASK, 1>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl,
-                                                  rs, r);
+        plane<T, S, NW, RPT, CPT, false, MASK, 1, TMA>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out,
+                                                       pl, rs, r, tm);
       }
       zz += 6;
     } else {
       q.zz = zz;
-      plane<T, S, NW, RPT, CPT, true, true, 0>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl, rs,
-                                               r);
+      plane<T, S, NW, RPT, CPT, true, true, 0, TMA>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl,
+                                                    rs, r, tm);
       if (zz + 1 > q.ze) break;
       q.zz = zz + 1;
-      plane<T, S, NW, RPT, CPT, true, true, 1>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl, rs,
-                                               r);
+      plane<T, S, NW, RPT, CPT, true, true, 1, TMA>(cur, prv, pp, pre, X, q, m, colout, colin, src_next, dst_out, pl,
+                                                    rs, r, tm);
       zz += 2;
     }
   }
@@ -272,9 +348,17 @@ __device__ __forceinline__ void sweep(Xchg<T, S, NW, RPT, CPT> &X, PlaneCtx q, i
 
 // Tile: (32 CPT) columns x (NW RPT) rows including the S-cell halo; warp w
 // owns rows RPT w .. RPT w + RPT - 1 (inner y-neighbours stay in registers).
-template <typename T, int S, int NW, int RPT, int CPT, int MINB>
+template <typename T, int S, int NW, int RPT, int CPT>
+constexpr size_t tile_smem(bool tma) {
+  return tma ? (sizeof(Xchg<T, S, NW, RPT, CPT>) + 127) / 128 * 128 + (size_t)TMA_D * 32 * CPT * NW * RPT * sizeof(T) +
+                   8 * TMA_D
+             : sizeof(Xchg<T, S, NW, RPT, CPT>);
+}
+
+template <typename T, int S, int NW, int RPT, int CPT, int MINB, bool TMA>
 __global__ void __launch_bounds__(32 * NW, MINB)
-fe3d_tile(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, int nz, T r, int tiles_x) {
+fe3d_tile(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, int nz, T r, int tiles_x,
+          const __grid_constant__ CUtensorMap tmap) {
   using X_t = Xchg<T, S, NW, RPT, CPT>;
   extern __shared__ __align__(16) unsigned char smraw[];
   X_t &X = *reinterpret_cast<X_t *>(smraw);
@@ -318,36 +402,97 @@ fe3d_tile(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   q.ze = min(z0 + ZC, nz) - 1 + S;
   // tiles wholly inside the domain skip the Dirichlet mask
   const bool tile_in = x0 >= 0 && x0 + W <= nx && y0 >= 0 && y0 + H <= ny;
-  if (tile_in) sweep<T, S, NW, RPT, CPT, false>(X, q, zs, m, colout, colin, src_col, dst_col, pl, nx, r);
-  else sweep<T, S, NW, RPT, CPT, true>(X, q, zs, m, colout, colin, src_col, dst_col, pl, nx, r);
+  TmaCtx tm{};
+  if constexpr (TMA) {
+    const uint32_t base = smem_addr(smraw);
+    tm.ring = base + (uint32_t)((sizeof(X_t) + 127) / 128 * 128);
+    tm.bars = tm.ring + (uint32_t)(TMA_D * W * H * sizeof(T));
+    tm.x0 = x0;
+    tm.y0 = y0;
+    tm.b = (int)blockIdx.z;
+    tm.zs = zs;
+    tm.map = &tmap;
+    if (threadIdx.x == 0) {
+      for (int d = 0; d < TMA_D; ++d) tma_bar_init(tm.bars + 8u * (uint32_t)d);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int d = 0; d < TMA_D && zs + d <= q.ze; ++d) tma_plane<W, H, T>(tm, d, zs + d);
+  }
+  if (tile_in) sweep<T, S, NW, RPT, CPT, false, TMA>(X, q, zs, m, colout, colin, src_col, dst_col, pl, nx, r, tm);
+  else sweep<T, S, NW, RPT, CPT, true, TMA>(X, q, zs, m, colout, colin, src_col, dst_col, pl, nx, r, tm);
 }
 
-template <typename T, int S, int NW, int RPT, int CPT, int MINB>
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PINT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) pint_throw(PINT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 4-D map of nb slices (x fastest), box = one plane of a W x H tile; zero OOB fill
+template <typename T>
+bool make_plane_map(CUtensorMap *m, const T *base, int nx, int ny, int nz, int64_t nb, int64_t stride, int W, int H) {
+  const uint64_t esz = sizeof(T);
+  if (((uintptr_t)base & 15u) || (nx * esz) % 16 || (stride * esz) % 16 || nb > 0x7fffffff) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz, (cuuint64_t)nb};
+  cuuint64_t strides[3] = {(cuuint64_t)nx * esz, (cuuint64_t)nx * ny * esz, (cuuint64_t)stride * esz};
+  cuuint32_t box[4] = {(cuuint32_t)W, (cuuint32_t)H, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult rc = tensor_map_encoder()(m, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                           4, const_cast<T *>(base), dims, strides, box, es,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS;
+}
+
+template <typename T, int S, int NW, int RPT, int CPT, int MINB, bool TMA>
 void launch_tile(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, int nz, T r, cudaStream_t st) {
   constexpr int BX = 32 * CPT - 2 * S, BY = NW * RPT - 2 * S;
   const int tiles_x = (nx + BX - 1) / BX, tiles_y = (ny + BY - 1) / BY;
   const unsigned tz = (unsigned)((nz + ZC - 1) / ZC);
-  const size_t smem = sizeof(Xchg<T, S, NW, RPT, CPT>);
-  auto kern = fe3d_tile<T, S, NW, RPT, CPT, MINB>;
-  PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
     const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
-    kern<<<dim3((unsigned)(tiles_x * tiles_y), tz, n), 32 * NW, smem, st>>>(in + b0 * stride, out + b0 * stride,
-                                                                            stride, nx, ny, nz, r, tiles_x);
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    const bool tma = TMA && make_plane_map<T>(&map, in + b0 * stride, nx, ny, nz, n, stride, 32 * CPT, NW * RPT);
+    if (tma) {
+      auto kern = fe3d_tile<T, S, NW, RPT, CPT, MINB, true>;
+      const size_t smem = tile_smem<T, S, NW, RPT, CPT>(true);
+      PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<dim3((unsigned)(tiles_x * tiles_y), tz, n), 32 * NW, smem, st>>>(in + b0 * stride, out + b0 * stride,
+                                                                              stride, nx, ny, nz, r, tiles_x, map);
+    } else {
+      // no TMA (variant without it, or a layout the tensor map cannot describe:
+      // rows or slice strides not multiples of 16 bytes)
+      auto kern = fe3d_tile<T, S, NW, RPT, CPT, MINB, false>;
+      const size_t smem = tile_smem<T, S, NW, RPT, CPT>(false);
+      PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<dim3((unsigned)(tiles_x * tiles_y), tz, n), 32 * NW, smem, st>>>(in + b0 * stride, out + b0 * stride,
+                                                                              stride, nx, ny, nz, r, tiles_x, map);
+    }
   }
   PINT_CUDA(cudaGetLastError());
 }
 
 // one pass of s <= SMAX levels
-template <typename T, int SMAX, int NW, int RPT, int CPT, int MINB>
+template <typename T, int SMAX, int NW, int RPT, int CPT, int MINB, bool TMA>
 void pass_tile(int s, const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, int nz, T r, cudaStream_t st) {
-  if constexpr (SMAX >= 4) if (s == 4) return launch_tile<T, 4, NW, RPT, CPT, MINB>(in, out, nb, stride, nx, ny, nz, r, st);
-  if constexpr (SMAX >= 3) if (s == 3) return launch_tile<T, 3, NW, RPT, CPT, MINB>(in, out, nb, stride, nx, ny, nz, r, st);
-  if constexpr (SMAX >= 2) if (s == 2) return launch_tile<T, 2, NW, RPT, CPT, MINB>(in, out, nb, stride, nx, ny, nz, r, st);
-  launch_tile<T, 1, NW, RPT, CPT, MINB>(in, out, nb, stride, nx, ny, nz, r, st);
+  if constexpr (SMAX >= 4) if (s == 4) return launch_tile<T, 4, NW, RPT, CPT, MINB, TMA>(in, out, nb, stride, nx, ny, nz, r, st);
+  if constexpr (SMAX >= 3) if (s == 3) return launch_tile<T, 3, NW, RPT, CPT, MINB, TMA>(in, out, nb, stride, nx, ny, nz, r, st);
+  if constexpr (SMAX >= 2) if (s == 2) return launch_tile<T, 2, NW, RPT, CPT, MINB, TMA>(in, out, nb, stride, nx, ny, nz, r, st);
+  launch_tile<T, 1, NW, RPT, CPT, MINB, TMA>(in, out, nb, stride, nx, ny, nz, r, st);
 }
 
-template <typename T, int SMAX, int NW, int RPT, int CPT, int MINB>
+template <typename T, int SMAX, int NW, int RPT, int CPT, int MINB, bool TMA = false>
 void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride, cudaStream_t st) {
   const int64_t S = op->desc.steps;
   const int64_t npass = (S + SMAX - 1) / SMAX;
@@ -357,7 +502,7 @@ void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, 
     const int s = (int)std::min<int64_t>(SMAX, S - done);
     const T *src = pass == 0 ? in : (((npass - pass) % 2 == 0) ? out : scratch);
     T *dstp = ((npass - 1 - pass) % 2 == 0) ? out : scratch;
-    pass_tile<T, SMAX, NW, RPT, CPT, MINB>(s, src, dstp, nb, stride, (int)op->nx, (int)op->ny, (int)op->nz, r, st);
+    pass_tile<T, SMAX, NW, RPT, CPT, MINB, TMA>(s, src, dstp, nb, stride, (int)op->nx, (int)op->ny, (int)op->nz, r, st);
     done += s;
   }
 }
@@ -370,8 +515,9 @@ void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, 
 //   fp32: 1 = S4 64x32 (NW32 RPT1), 2 = S3 64x32, 3 = S4 64x32 (NW16 RPT2), 4 = S4 64x48 (NW24 RPT2),
 //         5 = S2 128x32 (NW16 RPT2 CPT4), 6 = S3 64x32 (NW16 RPT2), 7 = S4 64x64 (NW32 RPT2),
 //         8 = S3 64x48 (NW16 RPT3), 9 = S4 64x36 (NW12 RPT3), 10 = S3 64x40 (NW20 RPT2), 11 = S4 64x40 (NW20 RPT2)
+//         12 = variant 8 with TMA input planes, 13 = variant 3 with TMA, 14 = variant 9 with TMA
 //   fp64: 1 = S4 64x16, 2 = S3 64x24, 3 = S3 64x20, 4 = S4 64x32 (NW16 RPT2), 5 = S3 64x32 (NW16 RPT2),
-//         6 = S2 64x32 (NW16 RPT2), 7 = S3 64x40 (NW20 RPT2)
+//         6 = S2 64x32 (NW16 RPT2), 7 = S3 64x40 (NW20 RPT2), 8 = variant 5 with TMA input planes
 // Defaults measured at the C4 shape (profiles/r01_fe3d_variants.jsonl).
 int fe3d_tile_default(int esz) { return esz == 4 ? 8 : 5; }
 
@@ -391,6 +537,9 @@ bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scr
       case 9: apply_tile<T, 4, 12, 3, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
       case 10: apply_tile<T, 3, 20, 2, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
       case 11: apply_tile<T, 4, 20, 2, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
+      case 12: apply_tile<T, 3, 16, 3, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 13: apply_tile<T, 4, 16, 2, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 14: apply_tile<T, 4, 12, 3, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       default: return false;
     }
   } else {
@@ -402,6 +551,7 @@ bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scr
       case 5: apply_tile<T, 3, 16, 2, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
       case 6: apply_tile<T, 2, 16, 2, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
       case 7: apply_tile<T, 3, 20, 2, 2, 1>(op, in, out, scratch, nb, stride, st); return true;
+      case 8: apply_tile<T, 3, 16, 2, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       default: return false;
     }
   }

@@ -272,7 +272,7 @@ class NativeAsyncDomain:
 def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | None = None, *,
                                    max_events: int = 200_000, delay_frac: float = 0.0, seed: int = 0,
                                    record_trace: bool = False, trace_cap: int | None = None,
-                                   domain_factory=None, coarse_init=None) -> dict:
+                                   domain_factory=None, coarse_init_rows=None, gather: bool = True) -> dict:
     """Asynchronous Parareal over all ranks (Algorithm 2; reference
     run_async_parareal, async_parareal.py:61-84), one domain of contiguous
     slices per GPU. The data path is peer memory only: each rank's kernel
@@ -281,11 +281,17 @@ def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | No
     outcome afterwards (stop code, non-finite flag, activation counts, the
     trace) and gathers the final iterate.
 
-    Returns {"final": (p+1) x N tensor on this rank's device (every rank),
-    "counts", "activations", "stop_reason", "kappa", "wall_s", "trace"}.
+    Memory per rank: only the rank's rows (lo-1 .. hi) of the coarse initial
+    iterate are formed (the chain from u0 is run up to hi with two working
+    rows), and the final iterate is gathered to rank 0 (``gather``) instead of
+    being assembled on every rank.
+
+    Returns {"rows": this rank's final slices lo..hi, "final": (p+1) x N
+    tensor on rank 0 when ``gather`` (None elsewhere), "counts",
+    "activations", "stop_reason", "kappa", "wall_s", "trace", "slices"}.
     ``domain_factory(coarse, fine, p, lo, hi, world, rank, trace_cap)`` and
-    ``coarse_init(coarse, u0, p) -> (p+1) x N tensor`` replace the native
-    pieces (the CPU tests drive the protocol with test doubles)."""
+    ``coarse_init_rows(coarse, u0, first, last) -> rows first..last`` replace
+    the native pieces (the CPU tests drive the protocol with test doubles)."""
     import time
 
     import numpy as np
@@ -298,9 +304,10 @@ def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | No
     if getattr(fine, "is_tridiagonal", False):
         from .model import with_register_layout
         coarse = with_register_layout(coarse, fine.info.points_per_thread)
-    if coarse_init is None:
-        coarse_init = _device_coarse_init
-    lam = coarse_init(coarse, u0, p)  # redundant on every rank: bitwise identical, no exchange
+    if coarse_init_rows is None:
+        from .async_mp import device_coarse_init_rows as coarse_init_rows
+    # rows lo-1 .. hi, chained from u0 on every rank: bitwise identical, no exchange
+    lam = coarse_init_rows(coarse, u0, lo - 1, hi)
     dev = lam.device
     cap = int(trace_cap if trace_cap is not None else min(max_events, 1_000_000)) if record_trace else 0
     factory = domain_factory or NativeAsyncDomain
@@ -311,7 +318,7 @@ def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | No
     dist.all_gather(allh, hb)
     handles = [bytes(t.cpu().tolist()) for t in allh]
     dom.connect(handles, [h_ - l_ + 1 for l_, h_ in parts])
-    dom.reset(lam[lo - 1:hi + 1].contiguous())
+    dom.reset(lam.contiguous())
     barrier()  # every mailbox and board is reset before any rank may push
     t0 = time.perf_counter()
     dom.launch(-1.0 if epsilon is None else float(epsilon), max_events, delay_frac, seed)
@@ -329,12 +336,7 @@ def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | No
     cnt = torch.zeros(p + 1, dtype=torch.int64, device=_red_device())
     cnt[lo:hi + 1] = torch.as_tensor(counts[1:], device=cnt.device)
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-    # final iterate: every rank contributes its owned rows (row 0 = u0 from rank 0)
-    full = torch.zeros(p + 1, lam.shape[1], dtype=lam.dtype, device=_red_device())
-    full[lo:hi + 1] = rows[1:].to(full.device)
-    if rank == 0:
-        full[0] = rows[0].to(full.device)
-    dist.all_reduce(full, op=dist.ReduceOp.SUM)
+    full = _gather_final(rows, parts, p, rank, world) if gather else None
     tr = None
     if cap > 0:
         tt = torch.as_tensor(trace, device=_red_device())
@@ -344,15 +346,27 @@ def run_async_parareal_distributed(coarse, fine, u0, p: int, epsilon: float | No
     if nonfinite:
         raise ValueError("block entries must be finite")
     counts_all = cnt.cpu().numpy()
-    out = {"final": full.to(dev), "counts": counts_all, "activations": int(info[0]),
+    out = {"rows": rows[1:], "final": None if full is None else full.to(dev), "counts": counts_all, "activations": int(info[0]),
            "stop_reason": {1: "converged", 2: "max_events"}.get(stop_code, "unknown"),
            "kappa": int(counts_all[1:].max()), "wall_s": wall_max, "trace": tr, "slices": (lo, hi)}
     return out
 
 
-def _device_coarse_init(coarse, u0, p: int) -> torch.Tensor:
-    from .parareal import _coarse_init_into, _u0_tensor
-    lam = torch.empty(p + 1, coarse.dim, dtype=coarse.dtype, device=f"cuda:{coarse.device}")
-    lam[0] = _u0_tensor(coarse, u0)
-    _coarse_init_into(coarse, lam, p, None)
-    return lam
+def _gather_final(rows: torch.Tensor, parts, p: int, rank: int, world: int):
+    """The final iterate on rank 0 only: every rank sends its owned rows
+    (padded to the largest shard so the collective has one shape); row 0 =
+    u0 from rank 0. Nothing of size (p+1) x N is allocated on other ranks."""
+    dev = _red_device()
+    width = max(h - l + 1 for l, h in parts)
+    mine = torch.zeros(width, rows.shape[1], dtype=rows.dtype, device=dev)
+    lo, hi = parts[rank]
+    mine[:hi - lo + 1] = rows[1:].to(dev)
+    bufs = [torch.empty_like(mine) for _ in range(world)] if rank == 0 else None
+    dist.gather(mine, gather_list=bufs, dst=0)
+    if rank != 0:
+        return None
+    full = torch.empty(p + 1, rows.shape[1], dtype=rows.dtype, device=dev)
+    full[0] = rows[0].to(dev)
+    for (l_, h_), b in zip(parts, bufs):
+        full[l_:h_ + 1] = b[:h_ - l_ + 1]
+    return full

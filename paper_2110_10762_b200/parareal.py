@@ -128,23 +128,53 @@ def coarse_init(coarse, u0, p: int) -> BlockVector:
     return BlockVector(lam, check_finite=False)
 
 
-def parareal_iterate(coarse, fine, lam: BlockVector) -> BlockVector:
+def parareal_iterate(coarse, fine, lam: BlockVector, out: torch.Tensor | None = None) -> BlockVector:
     """One full sweep over all interface states, ascending in i, component 0
-    pinned (parareal.py:66-76)."""
-    prev = lam.tensor.to(device=f"cuda:{fine.device}", dtype=fine.dtype)
-    p = prev.shape[0] - 1
-    new = prev.clone()
-    fv = fine.apply_batch(prev[:p])
-    g = torch.empty(1, fine.dim, dtype=fine.dtype, device=prev.device)
-    go = torch.empty_like(g)
-    for i in range(1, p + 1):
-        if torch.equal(new[i - 1], prev[i - 1]):
-            new[i] = fv[i - 1]
-            continue
-        coarse.apply_ptr(new[i - 1].data_ptr(), g.data_ptr(), 1, fine.dim)
-        coarse.apply_ptr(prev[i - 1].data_ptr(), go.data_ptr(), 1, fine.dim)
-        correct_into(fine, g, fv[i - 1:i], go, None, new[i:i + 1], None, None, None, 1)
-    return BlockVector(new, check_finite=False)
+    pinned (parareal.py:66-76): new[i] = parareal_update(G, F, new[i-1],
+    lam[i-1]) — the synchronous engine's sweep k = 1 with G(old) recomputed
+    from ``lam`` (bitwise one sweep of run_parareal).
+
+    Host in, host out: when ``lam`` holds a host tensor the sweep runs from
+    host buffers (pinned uploads overlapped with the F launches that read
+    them, results downloaded part by part as the coarse chain passes, the
+    stream work replayed as one CUDA graph) and the result is a host
+    BlockVector in ``out`` (a pinned (p+1) x N tensor, allocated when not
+    given). A device ``lam`` gives a device result."""
+    t = lam.tensor
+    p = t.shape[0] - 1
+    if p < 1:
+        raise ValueError(f"need p >= 1 subintervals, got {p}")
+    if t.shape[1] != fine.dim:
+        from .errors import DimensionError
+        raise DimensionError(f"block dim {t.shape[1]} does not match the propagator dim {fine.dim}")
+    eng = _iterate_engine(coarse, fine, p)
+    if t.device.type == "cpu":
+        host_in = t if (t.dtype == fine.dtype and t.is_pinned() and t.is_contiguous()) else \
+            t.to(fine.dtype).contiguous().pin_memory()
+        if out is None:
+            out = torch.empty_like(host_in).pin_memory()
+        out[0].copy_(host_in[0])
+        eng.prev = eng.lam_b
+        eng.sweep_host(1, host_in, out, graph=True, gold_from_prev=True)
+        return BlockVector(out, check_finite=False)
+    eng.lam_a.copy_(t.to(device=eng.lam_a.device, dtype=fine.dtype))
+    eng.lam_b[0].copy_(eng.lam_a[0])
+    eng.prev = eng.lam_a
+    eng.sweep(1, eng.lam_b, gold_from_prev=True)
+    eng.read_delta()  # raises ValueError on a non-finite state
+    return BlockVector(eng.lam_b.clone(), check_finite=False)
+
+
+def _iterate_engine(coarse, fine, p: int):
+    """A SyncEngine kept on the fine operator for repeated parareal_iterate
+    calls with the same (coarse, p) (buffers and captured graphs reused)."""
+    cache = fine.__dict__.setdefault("_iterate_engines", {})
+    key = (id(coarse), int(p))
+    eng = cache.get(key)
+    if eng is None:
+        cache.clear()
+        eng = cache[key] = SyncEngine(coarse, fine, p)
+    return eng
 
 
 @dataclass
@@ -279,7 +309,8 @@ class SyncEngine:
         return out
 
     def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, h2d=None, d2h=None,
-              d2h_splits: int = 1, h2d_splits: int = 1, speculate: bool = False) -> None:
+              d2h_splits: int = 1, h2d_splits: int = 1, speculate: bool = False,
+              gold_from_prev: bool = False) -> None:
         """Sweep k (device work only, stream-ordered): nxt <- new iterate.
         With several chunks, chunk c's coarse sweep overlaps chunk c+1's F.
         With h2d_splits > 1 every chunk's F is split into that many launches
@@ -295,8 +326,13 @@ class SyncEngine:
         sweep's first chunk has its new values (on its own stream, not joined
         into the current stream), so it runs while this sweep's chain finishes
         and the host reads the delta; the next ``sweep(k+1)`` uses it (a
-        stop at k discards it)."""
+        stop at k discards it).
+        gold_from_prev: G(old) is recomputed from the iterate (gcache[i] <-
+        G(prev[i-1]) next to each F launch) instead of taken from the previous
+        sweep — a standalone sweep (parareal_iterate)."""
         chunks = self.chunks(k)
+        if gold_from_prev:
+            speculate = False
         spec = getattr(self, "_spec", None)
         self._spec = None
         if spec is not None and (spec[0] != k or spec[1] is not self.prev or h2d is not None):
@@ -304,6 +340,9 @@ class SyncEngine:
             spec = None
         if len(chunks) == 1 and h2d is None and d2h is None and spec is None:
             self.fine_batch(k, fine_done_event)
+            if gold_from_prev:
+                self.coarse.apply_ptr(self.prev[k - 1].data_ptr(), self.gcache[k].data_ptr(), self.p - k + 1,
+                                      self.fine.dim)
             self.coarse_sweep(k, nxt)
             self.reduce_delta(k)
             self.prev = nxt
@@ -358,6 +397,9 @@ class SyncEngine:
                     st.wait_event(ev)
                 self.fine.apply_ptr(self.prev[pa - 1].data_ptr(), self.fv[pa].data_ptr(), pb - pa + 1, n,
                                     stream=st.cuda_stream)
+                if gold_from_prev:
+                    self.coarse.apply_ptr(self.prev[pa - 1].data_ptr(), self.gcache[pa].data_ptr(), pb - pa + 1, n,
+                                          stream=st.cuda_stream)
                 ev = torch.cuda.Event()
                 ev.record(st)
                 evs.append(ev)
@@ -435,7 +477,7 @@ class SyncEngine:
         return subs[q]
 
     def sweep_host(self, k: int, host_prev: torch.Tensor, host_next: torch.Tensor, d2h_splits: int = 4,
-                   h2d_splits: int = 8, graph: bool = False) -> float:
+                   h2d_splits: int = 8, graph: bool = False, gold_from_prev: bool = False) -> float:
         """One sweep from host (pinned) buffers: host_prev -> device iterate ->
         sweep -> host_next. Uploads run ahead of the F launches that read
         them; with h2d_splits > 1 each chunk's F runs as that many launches
@@ -449,17 +491,18 @@ class SyncEngine:
         dev_prev = self.lam_a if self.prev is not self.lam_a else self.lam_b
         nxt = self.lam_b if dev_prev is self.lam_a else self.lam_a
         if graph:
-            key = (k, host_prev.data_ptr(), host_next.data_ptr(), d2h_splits, h2d_splits, dev_prev is self.lam_a)
+            key = (k, host_prev.data_ptr(), host_next.data_ptr(), d2h_splits, h2d_splits, dev_prev is self.lam_a,
+                   gold_from_prev)
             graphs = self.__dict__.setdefault("_graphs", {})
             g = graphs.get(key)
             if g is None:
                 g = self._capture(lambda: self._host_sweep_work(k, dev_prev, nxt, host_prev, host_next, d2h_splits,
-                                                                h2d_splits))
+                                                                h2d_splits, gold_from_prev))
                 graphs[key] = g
             g.replay()
             self.prev = nxt
         else:
-            self._host_sweep_work(k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits)
+            self._host_sweep_work(k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits, gold_from_prev)
         torch.cuda.current_stream(self.fine.device).synchronize()
         if self.host[1].item() != 0.0:
             raise ValueError("block entries must be finite")
@@ -477,7 +520,8 @@ class SyncEngine:
         torch.cuda.current_stream(dev).wait_stream(cap)
         return g
 
-    def _host_sweep_work(self, k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits) -> None:
+    def _host_sweep_work(self, k, dev_prev, nxt, host_prev, host_next, d2h_splits, h2d_splits,
+                         gold_from_prev=False) -> None:
 
         def h2d(r0, r1, st):
             with torch.cuda.stream(st):
@@ -491,7 +535,8 @@ class SyncEngine:
                     self.host[1:2].copy_(self.flag.to(torch.float64), non_blocking=True)
 
         self.prev = dev_prev
-        self.sweep(k, nxt, h2d=h2d, d2h=d2h, d2h_splits=d2h_splits, h2d_splits=h2d_splits)
+        self.sweep(k, nxt, h2d=h2d, d2h=d2h, d2h_splits=d2h_splits, h2d_splits=h2d_splits,
+                   gold_from_prev=gold_from_prev)
 
     def launches_per_sweep(self, k: int = 1) -> int:
         """Our kernel launches per sweep (fused path: F batch and coarse sweep

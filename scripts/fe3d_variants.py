@@ -18,7 +18,9 @@ if __name__ == "__main__":
     p = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 24
     n = int(os.environ.get("FE3D_N", 256))
-    variants = [0, 3, 6, 8, 9, 10, 11] if dtype == "float32" else [0, 2, 4, 5, 6, 7]
+    variants = [0, 3, 6, 8, 9, 12, 13, 14] if dtype == "float32" else [0, 4, 5, 7, 8]
+    if os.environ.get("FE3D_VARIANTS"):
+        variants = [int(v) for v in os.environ["FE3D_VARIANTS"].split(",")]
     h = 1.0 / (n + 1)
     ivp = pb.heat3d_system(n, t_final=1.0)
     g = torch.Generator(device="cuda").manual_seed(0)

@@ -165,16 +165,17 @@ def _async_worker(rank, world, port, p, out):
         d.u0 = u0
         return d
 
-    def cinit(c, u, pp):
-        lam = np.zeros((pp + 1, len(u)))
+    def cinit_rows(c, u, first, last):
+        lam = np.zeros((last + 1, len(u)))
         lam[0] = u
-        for i in range(1, pp + 1):
+        for i in range(1, last + 1):
             lam[i] = c.apply(lam[i - 1])
-        return torch.from_numpy(lam)
+        return torch.from_numpy(lam[first:])
 
     res = D.run_async_parareal_distributed(coarse, fine, u0, p, None, record_trace=True, trace_cap=p,
-                                           domain_factory=factory, coarse_init=cinit)
-    np.savez(out + f".{rank}.npz", final=res["final"].numpy(), counts=res["counts"], trace=res["trace"],
+                                           domain_factory=factory, coarse_init_rows=cinit_rows)
+    final = res["final"].numpy() if res["final"] is not None else np.zeros(0)
+    np.savez(out + f".{rank}.npz", final=final, rows=res["rows"].numpy(), counts=res["counts"], trace=res["trace"],
              stop=res["stop_reason"], kappa=res["kappa"], slices=np.array(res["slices"]))
     dist.destroy_process_group()
 
@@ -190,7 +191,12 @@ def test_async_distributed_protocol(tmp_path, world, p):
     parts = async_partition(p, world)
     for r in range(world):
         got = np.load(out + f".{r}.npz")
-        assert np.array_equal(got["final"], seq)  # every rank holds the assembled iterate
+        lo, hi = parts[r]
+        assert np.array_equal(got["rows"], seq[lo:hi + 1])  # each rank holds only its own slices
+        if r == 0:
+            assert np.array_equal(got["final"], seq)  # gathered to rank 0
+        else:
+            assert got["final"].size == 0
         assert np.array_equal(got["counts"], np.r_[0, np.ones(p, dtype=np.int64)])
         assert str(got["stop"]) == "converged" and int(got["kappa"]) == 1
         assert tuple(got["slices"]) == parts[r]
