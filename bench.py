@@ -657,14 +657,36 @@ def multi_gpu_time_to_tolerance(rank: int, world: int) -> dict:
     return out
 
 
-def _launch_ranks(n: int) -> int:
+def dry_run(rank: int, world: int) -> None:
+    """The rank layout of an N-GPU run without GPU work (gloo): which slices
+    every rank owns in the weak-scaling sync bench and in the async runs."""
+    import torch.distributed as dist
+
+    from paper_2110_10762_b200.distributed import async_partition
+    if world > 1:
+        dist.init_process_group("gloo")
+    info = {"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", 0)), "pid": os.getpid()}
+    ranks = [None] * world
+    if world > 1:
+        dist.all_gather_object(ranks, info)
+        dist.destroy_process_group()
+    else:
+        ranks = [info]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks,
+                          "sync_c2_slices": [[r * P_LOCAL + 1, (r + 1) * P_LOCAL] for r in range(world)],
+                          "async_c2_partition": async_partition(P_LOCAL, world),
+                          "async_c4_partition": async_partition(ND_CONFIGS["c4_f32"]["p"], world)}), flush=True)
+
+
+def _launch_ranks(n: int, check_devices: bool = True) -> int:
     """Re-run this command under torchrun, one rank per GPU (127.0.0.1)."""
     import socket
     import subprocess
 
     import torch
     have = torch.cuda.device_count()
-    if have < n:
+    if check_devices and have < n:
         sys.stderr.write(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible\n")
         return 2
     with socket.socket() as sk:
@@ -688,6 +710,8 @@ def main():
     ap.add_argument("--configs", action="store_true", default=True,
                     help="C3/C4/C5 lines (2-D/3-D fine throughput, time to tolerance, CPU port) (default on)")
     ap.add_argument("--no-configs", dest="configs", action="store_false")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the N ranks (gloo, no GPU work) and print the rank layout")
     args = ap.parse_args()
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
@@ -698,10 +722,13 @@ def main():
         run_reference(args, rank, int(world_env) if world_env else args.gpus)
         return
     if world_env is None and args.gpus > 1:
-        sys.exit(_launch_ranks(args.gpus))
+        sys.exit(_launch_ranks(args.gpus, check_devices=not args.dry_run))
     world = int(world_env) if world_env else 1
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        dry_run(rank, world)
+        return
     if world > 1:
         from paper_2110_10762_b200 import distributed as dist_rt
         dist_rt.init_process_group()
