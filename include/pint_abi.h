@@ -269,6 +269,14 @@ int pint_mailbox_read(pint_ctx *ctx, const void *ring, int64_t slot_bytes, int64
                       int64_t *v_out, int32_t *torn, void *stream);
 
 /*
+ * Stream-ordered wait until *ver >= value (a version another GPU publishes
+ * with pint_mailbox_push): one thread polls with system-scope acquire loads;
+ * after timeout_s it sets *timed_out = 1 and returns instead of hanging.
+ */
+int pint_mailbox_wait(pint_ctx *ctx, const int64_t *ver, int64_t value, double timeout_s,
+                      int32_t *timed_out, void *stream);
+
+/*
  * Status boards: slot = 8 int64 {seq, w0..w6}; post writes seq+1, the seven
  * words, seq+2 (system-scope release); read snapshots nslots slots with
  * acquire loads until both sequence reads agree (seq -1 if a slot never

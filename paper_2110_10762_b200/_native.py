@@ -104,6 +104,7 @@ SIGNATURES = {
     "pint_mailbox_push": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "pint_mailbox_read": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_void_p, c_i64, c_void_p, c_void_p,
                                   c_void_p, c_void_p]),
+    "pint_mailbox_wait": (c_int, [c_void_p, c_void_p, c_i64, c_double, c_void_p, c_void_p]),
     "pint_board_post": (c_int, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "pint_board_read": (c_int, [c_void_p, c_void_p, c_i32, c_void_p, c_void_p]),
     "pint_tri1d_plan_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -172,6 +172,12 @@ class CudaTransport:
         with torch.cuda.stream(stream):
             torch.cuda._sleep(int(cycles))
 
+    def wait_version(self, ver_ptr: int, value: int, timed_out: torch.Tensor, stream, timeout_s: float = 30.0) -> None:
+        """Stream-ordered wait (one-thread device poll) for a peer's version."""
+        self._chk(self.lib.pint_mailbox_wait(self.ctx, ctypes.c_void_p(ver_ptr), int(value), float(timeout_s),
+                                             ctypes.c_void_p(timed_out.data_ptr()), self.sptr(stream)),
+                  "pint_mailbox_wait")
+
     def synchronize(self) -> None:
         torch.cuda.synchronize(self.device)
 

@@ -67,6 +67,25 @@ __global__ void __launch_bounds__(256) push_kernel(uint4 *__restrict__ dst, cons
 
 __global__ void pick_kernel(const long long *ver, long long *vsel) { *vsel = ld_acq_sys(ver); }
 
+// Stream-ordered wait for a version published by another GPU (the chain edge
+// of the synchronous multi-GPU sweep): one thread polls with acquire loads;
+// gives up after timeout_ns (globaltimer) and flags it instead of hanging.
+__global__ void wait_kernel(const long long *ver, long long value, unsigned long long timeout_ns, int32_t *timed_out) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  while (ld_acq_sys(ver) < value) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      *timed_out = 1;
+      return;
+    }
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : ns;
+  }
+}
+
 __global__ void __launch_bounds__(256) read_kernel(uint4 *__restrict__ dst, const unsigned char *ring,
                                                    int64_t slot_bytes, int64_t nslots, const long long *vsel,
                                                    int64_t n16, unsigned char *dtail, int tail) {
@@ -202,6 +221,16 @@ int pint_mailbox_read(pint_ctx *ctx, const void *ring, int64_t slot_bytes, int64
                                               (const long long *)vsel, n16, (unsigned char *)dst + n16 * 16, tail);
     validate_kernel<<<1, 1, 0, s>>>((const long long *)ver, (const long long *)vsel, nslots, (long long *)v_out,
                                     torn);
+    PINT_CUDA(cudaGetLastError());
+  });
+}
+
+int pint_mailbox_wait(pint_ctx *ctx, const int64_t *ver, int64_t value, double timeout_s, int32_t *timed_out,
+                      void *stream) {
+  if (!ctx || !ver || !timed_out || !(timeout_s > 0.0)) return PINT_EARG;
+  return pint_guarded(ctx, [&] {
+    wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const long long *)ver, (long long)value,
+                                                   (unsigned long long)(timeout_s * 1e9), timed_out);
     PINT_CUDA(cudaGetLastError());
   });
 }

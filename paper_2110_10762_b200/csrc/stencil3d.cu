@@ -43,6 +43,16 @@ constexpr int TMA_D = 4;  // input planes in flight per CTA (TMA ring depth)
 // (4-D tensor map x, y, z, slice; the halo outside the grid is zero-filled by
 // the TMA unit, i.e. the zero Dirichlet values), TMA_D planes ahead of the
 // wavefront, each completing on its own mbarrier.
+// x extent of a tile: halo HL on the left, BX output columns. With TMA the
+// box origin x0 must be a multiple of 16 bytes (the unit refuses other inner
+// coordinates), so the TMA tilings use 4-column halos (x0 = 56 bx - 4 is a
+// multiple of 4 floats / 2 doubles; S <= 4 levels fit in the halo).
+template <int S, int CPT, bool TMA>
+struct XTile {
+  static constexpr int HL = TMA ? 4 : S;
+  static constexpr int BX = 32 * CPT - HL - (TMA ? 4 : S);
+};
+
 struct TmaCtx {
   uint32_t ring;  // shared address of slot 0
   uint32_t bars;  // shared address of TMA_D mbarriers
@@ -363,10 +373,10 @@ fe3d_tile(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   extern __shared__ __align__(16) unsigned char smraw[];
   X_t &X = *reinterpret_cast<X_t *>(smraw);
   constexpr int W = 32 * CPT, H = NW * RPT;
-  constexpr int BX = W - 2 * S, BY = H - 2 * S;
+  constexpr int BX = XTile<S, CPT, TMA>::BX, HL = XTile<S, CPT, TMA>::HL, BY = H - 2 * S;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
-  const int x0 = bx * BX - S, y0 = by * BY - S, z0 = blockIdx.y * ZC;
+  const int x0 = bx * BX - HL, y0 = by * BY - S, z0 = blockIdx.y * ZC;
   const int64_t pl = (int64_t)nx * ny;
   const int cx = x0 + CPT * lane, cy0 = y0 + RPT * w;
   T m[RPT][CPT];
@@ -378,7 +388,7 @@ fe3d_tile(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
       const int cy = cy0 + y, ly = RPT * w + y, lx = CPT * lane + c;
       colin[y][c] = cx + c >= 0 && cx + c < nx && cy >= 0 && cy < ny;
       m[y][c] = colin[y][c] ? T(1) : T(0);
-      colout[y][c] = colin[y][c] && lx >= S && lx < S + BX && ly >= S && ly < S + BY;
+      colout[y][c] = colin[y][c] && lx >= HL && lx < HL + BX && ly >= S && ly < S + BY;
     }
   {
     using V = typename Vec<T, CPT>::V;
@@ -456,14 +466,19 @@ bool make_plane_map(CUtensorMap *m, const T *base, int nx, int ny, int nz, int64
 
 template <typename T, int S, int NW, int RPT, int CPT, int MINB, bool TMA>
 void launch_tile(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, int nz, T r, cudaStream_t st) {
-  constexpr int BX = 32 * CPT - 2 * S, BY = NW * RPT - 2 * S;
+  constexpr int BY = NW * RPT - 2 * S;
+  // the TMA tiling has its own x step; a layout the tensor map cannot describe
+  // runs the non-TMA kernel with the non-TMA step
+  const bool tma_ok = TMA && ((uintptr_t)in & 15u) == 0 && (nx * sizeof(T)) % 16 == 0 && (stride * sizeof(T)) % 16 == 0;
+  const int BX = tma_ok ? XTile<S, CPT, true>::BX : XTile<S, CPT, false>::BX;
   const int tiles_x = (nx + BX - 1) / BX, tiles_y = (ny + BY - 1) / BY;
   const unsigned tz = (unsigned)((nz + ZC - 1) / ZC);
   for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
     const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
     CUtensorMap map;
     memset(&map, 0, sizeof(map));
-    const bool tma = TMA && make_plane_map<T>(&map, in + b0 * stride, nx, ny, nz, n, stride, 32 * CPT, NW * RPT);
+    const bool tma = tma_ok && make_plane_map<T>(&map, in + b0 * stride, nx, ny, nz, n, stride, 32 * CPT, NW * RPT);
+    if (tma_ok && !tma) pint_throw(PINT_ECUDA, "cuTensorMapEncodeTiled refused the plane map");
     if (tma) {
       auto kern = fe3d_tile<T, S, NW, RPT, CPT, MINB, true>;
       const size_t smem = tile_smem<T, S, NW, RPT, CPT>(true);
@@ -518,8 +533,10 @@ void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, 
 //         12 = variant 8 with TMA input planes, 13 = variant 3 with TMA, 14 = variant 9 with TMA
 //   fp64: 1 = S4 64x16, 2 = S3 64x24, 3 = S3 64x20, 4 = S4 64x32 (NW16 RPT2), 5 = S3 64x32 (NW16 RPT2),
 //         6 = S2 64x32 (NW16 RPT2), 7 = S3 64x40 (NW20 RPT2), 8 = variant 5 with TMA input planes
-// Defaults measured at the C4 shape (profiles/r01_fe3d_variants.jsonl).
-int fe3d_tile_default(int esz) { return esz == 4 ? 8 : 5; }
+// Defaults measured at the C4 shape (profiles/r02_fe3d_variants.jsonl): the
+// TMA input ring, fp32 948 -> 1109 GPt/s (variant 8 -> 12), fp64 457 -> 600
+// (variant 5 -> 8); 512^3 fp32 1178 -> 1272.
+int fe3d_tile_default(int esz) { return esz == 4 ? 12 : 8; }
 
 template <typename T>
 bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride,

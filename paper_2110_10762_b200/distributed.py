@@ -12,10 +12,25 @@ Algorithm 1, and parareal.py:119-127):
   4. send the last local slice's new value and delta to rank r+1;
   5. one 16-byte MAX all-reduce of (delta, non-finite flag).
 
+Wavefront overlap (Algorithm 1: "processor i-1 starts
+applying F before processor i"): as soon as rank r's own chain segment of
+sweep k is done, F of sweep k+1 over its slices is launched on a side stream
+(its inputs are all local by then: the rank's new rows and the boundary row
+received in step 2), so it runs while the downstream ranks are still in
+their chain of sweep k and while the delta is reduced; a stop at k discards
+it (``finish``).
+
 The only data-path exchange is the 1-D chain edge lambda_{i-1} -> lambda_i
-that crosses each GPU boundary once per sweep: one N*8-byte
-NCCL send/recv. Everything else stays on the owning GPU. The inner engine is
-pluggable so the protocol is unit-tested on CPU with gloo.
+that crosses each GPU boundary once per sweep. By default it
+goes over peer memory (``MailboxEdge``, K7): rank r's GPU pushes the boundary
+slice and its delta straight into rank r+1's mailbox with SM stores and a
+system-scope release of the sweep number (``pint_mailbox_push``), and rank
+r+1's stream waits for that version with a one-thread device poll
+(``pint_mailbox_wait``; a host poll when two ranks share a device, e.g. the
+one-GPU tests) before its chain — no NCCL on the data path. ``edge="nccl"``
+keeps the NCCL send/recv. Everything else stays on the owning GPU. The inner
+engine and the transport are pluggable so the protocol is unit-tested on CPU
+with gloo.
 """
 from __future__ import annotations
 
@@ -58,11 +73,85 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+class MailboxEdge:
+    """The chain edge of the sharded synchronous sweep over peer memory.
+    Two slots of [boundary row | its delta] in every rank's shared workspace,
+    guarded by one version word = the message sequence number (1 = the coarse
+    initial value, then one per sweep; both ends count their messages, so
+    repeated sweeps with the same k — the bench — stay ordered). A slot is
+    rewritten two messages later, after the per-sweep delta all-reduce that
+    the consumer can only pass once it has read it — so no flow control."""
+
+    def __init__(self, like: torch.Tensor, rank: int, world: int, transport, exchange, wait: str = "auto"):
+        self.tp, self.rank, self.world = transport, rank, world
+        n, dt = like.shape[-1], like.dtype
+        esz = like.element_size()
+        self.row_pad = (n * esz + 255) // 256 * 256
+        self.slot = self.row_pad + 256
+        self.ws = transport.alloc(256 + 2 * self.slot)
+        self.ver = transport.view(self.ws, (1,), torch.int64)
+        self.rows = [transport.view(self.ws + 256 + q * self.slot, (n,), dt) for q in range(2)]
+        self.dls = [transport.view(self.ws + 256 + q * self.slot + self.row_pad, (1,), torch.float64)
+                    for q in range(2)]
+        dev = like.device
+        self.stage = torch.zeros(self.slot, dtype=torch.uint8, device=dev)
+        self.stage_row = self.stage[:n * esz].view(dt)
+        self.stage_dl = self.stage[self.row_pad:self.row_pad + 8].view(torch.float64)
+        self.ctr = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.word_host = torch.zeros(1, dtype=torch.int64, pin_memory=dev.type == "cuda")
+        handle = transport.export(self.ws)
+        handles = exchange.all_gather_bytes(handle)
+        self.peer_next = transport.open(handles[rank + 1], self.ws, handle) if rank + 1 < world else None
+        if wait == "auto":
+            import socket
+            where = exchange.all_gather_object((socket.gethostname(), str(dev)))
+            wait = "device" if dev.type == "cuda" and len(set(where)) == world else "host"
+        self.wait = wait
+        self.sent = 0
+        self.received = 0
+
+    def recv(self, k: int, row0: torch.Tensor, delta0: torch.Tensor) -> None:
+        """Consumer: this sweep's new boundary row and delta from rank-1
+        (k = 0: the coarse initial value); message sequence numbers 1, 2, ..."""
+        self.received += 1
+        k = self.received
+        if self.wait == "device":
+            self.tp.wait_version(self.ver.data_ptr(), k, self.timed_out, torch.cuda.current_stream(row0.device))
+        else:
+            st = torch.cuda.current_stream(row0.device) if row0.device.type == "cuda" else None
+            while self.tp.read_word(self.ver, self.word_host, st) < k:
+                pass
+        q = k % 2
+        row0.copy_(self.rows[q])
+        delta0.copy_(self.dls[q])
+
+    def send(self, k: int, row: torch.Tensor, delta: torch.Tensor) -> None:
+        """Producer: push the boundary row and delta into rank+1's slot k % 2,
+        then publish its sequence number (SM stores + system-scope release)."""
+        self.sent += 1
+        k = self.sent
+        self.stage_row.copy_(row)
+        self.stage_dl.copy_(delta)
+        st = torch.cuda.current_stream(row.device) if row.device.type == "cuda" else None
+        self.tp.push(self.peer_next + 256 + (k % 2) * self.slot, self.stage, self.peer_next, k, self.ctr.data_ptr(),
+                     st)
+
+    def check(self) -> None:
+        if int(self.timed_out.item()) != 0:
+            raise RuntimeError("chain edge: the previous rank's boundary state did not arrive (mailbox wait timed out)")
+
+    def close(self) -> None:
+        self.tp.close()
+
+
 class ShardedSyncEngine:
     """One rank's share of the synchronous iteration. ``engine`` provides the
-    local device work (default: parareal.SyncEngine on this rank's GPU)."""
+    local device work (default: parareal.SyncEngine on this rank's GPU);
+    ``edge`` the chain edge ("mailbox": peer memory, K7; "nccl": send/recv;
+    or a MailboxEdge built with a test transport)."""
 
-    def __init__(self, coarse, fine, p_local: int, rank: int, world: int, engine=None):
+    def __init__(self, coarse, fine, p_local: int, rank: int, world: int, engine=None, edge="mailbox"):
         if engine is None:
             from .parareal import SyncEngine
             engine = SyncEngine(coarse, fine, p_local)
@@ -71,7 +160,15 @@ class ShardedSyncEngine:
         self.rank = int(rank)
         self.world = int(world)
         dev = self.eng.lam_a.device
-        self._red = torch.zeros(2, dtype=torch.float64, device=dev)
+        # the per-sweep reduction lives where the process group reduces (NCCL: the GPU; gloo: the host)
+        red_dev = _red_device() if dist.is_initialized() else dev
+        self._red = torch.zeros(2, dtype=torch.float64, device=red_dev)
+        self._spec = None
+        self._side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+        if edge == "mailbox" and world > 1:
+            from .async_mp import CudaTransport, TorchExchange
+            edge = MailboxEdge(self.eng.lam_a[0], rank, world, CudaTransport(fine), TorchExchange())
+        self.edge = edge if isinstance(edge, MailboxEdge) else None
 
     # views of the inner engine (bench resets the iterate through these)
     @property
@@ -99,26 +196,67 @@ class ShardedSyncEngine:
         if self.rank == 0:
             eng.init(u0)
         else:
-            dist.recv(eng.lam_a[0], src=self.rank - 1)
+            if self.edge is not None:
+                self.edge.recv(0, eng.lam_a[0], eng.deltas[0:1])
+            else:
+                dist.recv(eng.lam_a[0], src=self.rank - 1)
             eng.init(eng.lam_a[0])
         if self.rank + 1 < self.world:
-            dist.send(eng.lam_a[self.p].contiguous(), dst=self.rank + 1)
+            if self.edge is not None:
+                self.edge.send(0, eng.lam_a[self.p], eng.deltas[self.p:self.p + 1])
+            else:
+                dist.send(eng.lam_a[self.p].contiguous(), dst=self.rank + 1)
 
-    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None) -> None:
-        """Global sweep k on this rank's shard; nxt receives the new iterate."""
+    def _k_loc(self, k: int) -> int:
+        return max(1, k - self.rank * self.p)
+
+    def _launch_spec(self, k_loc: int):
+        """F of the next sweep over this rank's live slices, off the critical path."""
+        if self._side is None:  # host engine (tests): runs in order
+            self.eng.fine_batch(k_loc)
+            return None
+        main = torch.cuda.current_stream(self._side.device)
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            self.eng.fine_batch(k_loc)
+        ev = torch.cuda.Event()
+        ev.record(self._side)
+        return ev
+
+    def finish(self) -> None:
+        """Join a speculative F the run did not use (its buffers stay alive)."""
+        spec, self._spec = self._spec, None
+        if spec is not None and spec[1] is not None:
+            torch.cuda.current_stream(self._side.device).wait_event(spec[1])
+
+    def sweep(self, k: int, nxt: torch.Tensor, fine_done_event=None, speculate: bool = False) -> None:
+        """Global sweep k on this rank's shard; nxt receives the new iterate.
+        speculate: launch sweep k+1's F right after this rank's chain."""
         eng = self.eng
-        k_loc = max(1, k - self.rank * self.p)
+        k_loc = self._k_loc(k)
         live = k_loc <= self.p
+        spec, self._spec = self._spec, None
         if live:
-            eng.fine_batch(k_loc, fine_done_event)
+            if spec is not None and spec[0] == k:
+                if spec[1] is not None:
+                    torch.cuda.current_stream(self._side.device).wait_event(spec[1])
+                if fine_done_event is not None:
+                    fine_done_event.record()
+            else:
+                if spec is not None and spec[1] is not None:
+                    torch.cuda.current_stream(self._side.device).wait_event(spec[1])
+                eng.fine_batch(k_loc, fine_done_event)
         elif fine_done_event is not None:
             fine_done_event.record()
         chain_in = False
         if self.rank > 0:
-            w1 = dist.irecv(nxt[0], src=self.rank - 1)
-            w2 = dist.irecv(eng.deltas[0:1], src=self.rank - 1)
-            w1.wait()
-            w2.wait()
+            if self.edge is not None:
+                self.edge.recv(k, nxt[0], eng.deltas[0:1])
+            else:
+                w1 = dist.irecv(nxt[0], src=self.rank - 1)
+                w2 = dist.irecv(eng.deltas[0:1], src=self.rank - 1)
+                w1.wait()
+                w2.wait()
             chain_in = k_loc == 1
         if live:
             eng.coarse_sweep(k_loc, nxt, chain_in=chain_in)
@@ -127,17 +265,26 @@ class ShardedSyncEngine:
             nxt.copy_(eng.prev)
             eng.deltas.zero_()
             eng.dmax.zero_()
+        if speculate and self._k_loc(k + 1) <= self.p:
+            # this rank's rows of sweep k are final: F(k+1) can start now
+            eng.prev = nxt
+            self._spec = (k + 1, self._launch_spec(self._k_loc(k + 1)))
         if self.rank + 1 < self.world:
-            s1 = dist.isend(nxt[self.p].contiguous(), dst=self.rank + 1)
-            s2 = dist.isend(eng.deltas[self.p:self.p + 1].contiguous(), dst=self.rank + 1)
-            s1.wait()
-            s2.wait()
+            if self.edge is not None:
+                self.edge.send(k, nxt[self.p], eng.deltas[self.p:self.p + 1])
+            else:
+                s1 = dist.isend(nxt[self.p].contiguous(), dst=self.rank + 1)
+                s2 = dist.isend(eng.deltas[self.p:self.p + 1].contiguous(), dst=self.rank + 1)
+                s1.wait()
+                s2.wait()
         self._red[0:1].copy_(eng.dmax)
         self._red[1:2].copy_(eng.flag.to(torch.float64))
         dist.all_reduce(self._red, op=dist.ReduceOp.MAX)
         eng.prev = nxt
 
     def read_delta(self) -> float:
+        if self.edge is not None:
+            self.edge.check()
         vals = self._red.to("cpu")
         if vals[1] != 0.0:
             raise ValueError("block entries must be finite")
@@ -145,7 +292,7 @@ class ShardedSyncEngine:
 
 
 def run_parareal_sharded(coarse, fine, u0, p_local: int, epsilon: float, k_max: int | None = None,
-                         engine=None) -> dict:
+                         engine=None, edge="mailbox") -> dict:
     """Synchronous Parareal over all ranks (P = p_local * world slices) with
     the reference's stop rules (parareal.py:99-138). Returns this rank's final
     shard and the global stop bookkeeping."""
@@ -156,24 +303,27 @@ def run_parareal_sharded(coarse, fine, u0, p_local: int, epsilon: float, k_max: 
     cap = p if k_max is None else min(int(k_max), p)
     if cap < 1:
         raise ValueError(f"iteration budget must allow k >= 1, got k_max={k_max}")
-    sh = ShardedSyncEngine(coarse, fine, p_local, rank, world, engine=engine)
+    sh = ShardedSyncEngine(coarse, fine, p_local, rank, world, engine=engine, edge=edge)
     sh.init(u0)
     deltas, k, stop = [], 0, "k_max"
-    while k < cap:
-        k += 1
-        nxt = sh.lam_b if sh.prev is sh.lam_a else sh.lam_a
-        sh.sweep(k, nxt)
-        d = sh.read_delta()
-        deltas.append(d)
-        if d < epsilon:
-            stop = "threshold"
-            break
-        if k == p:
-            stop = "exact"
-            break
-        if k == cap:
-            stop = "k_max"
-            break
+    try:
+        while k < cap:
+            k += 1
+            nxt = sh.lam_b if sh.prev is sh.lam_a else sh.lam_a
+            sh.sweep(k, nxt, speculate=k < cap)
+            d = sh.read_delta()
+            deltas.append(d)
+            if d < epsilon:
+                stop = "threshold"
+                break
+            if k == p:
+                stop = "exact"
+                break
+            if k == cap:
+                stop = "k_max"
+                break
+    finally:
+        sh.finish()
     return {"k_final": k, "stop_reason": stop, "deltas": deltas, "shard": sh.prev.clone()}
 
 

@@ -63,12 +63,21 @@ def problem(n=64):
     return H.Tridiag1D(n, a_d, a_o, c, 0.05, 1), H.Tridiag1D(n, a_d, a_o, c, 0.05, 20), H.sine_u0_1d(n, 8, 0)
 
 
-def _worker(rank, world, port, p_local, eps, out):
+def _worker(rank, world, port, p_local, eps, out, edge="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2110_10762_b200 import distributed as D
     coarse, fine, u0 = problem()
-    res = D.run_parareal_sharded(coarse, fine, u0, p_local, eps, engine=CPUEngine(coarse, fine, p_local))
+    eng = CPUEngine(coarse, fine, p_local)
+    if edge == "mailbox":
+        # the peer-memory chain edge (K7) over the shared-memory test transport
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from async_mp_doubles import ShmTransport
+
+        from paper_2110_10762_b200.async_mp import TorchExchange
+        edge = D.MailboxEdge(eng.lam_a[0], rank, world, ShmTransport(), TorchExchange(), wait="host")
+    res = D.run_parareal_sharded(coarse, fine, u0, p_local, eps, engine=eng, edge=edge)
     shards = [torch.zeros_like(res["shard"]) for _ in range(world)]
     dist.all_gather(shards, res["shard"])
     if rank == 0:
@@ -85,10 +94,11 @@ def _free_port():
     return port
 
 
+@pytest.mark.parametrize("edge", ["nccl", "mailbox"])
 @pytest.mark.parametrize("world,p_local,eps", [(2, 4, 1e-9), (3, 3, 0.0), (2, 5, 1e-4)])
-def test_sharded_run_equals_single_process(tmp_path, world, p_local, eps):
+def test_sharded_run_equals_single_process(tmp_path, world, p_local, eps, edge):
     out = str(tmp_path / "res.npz")
-    mp.start_processes(_worker, args=(world, _free_port(), p_local, eps, out), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), p_local, eps, out, edge), nprocs=world, join=True,
                        start_method="spawn")
     got = np.load(out)
     coarse, fine, u0 = problem()

@@ -148,3 +148,53 @@ def test_two_processes_ipc_mailbox_quiescence_bitwise(gpu, tmp_path, dtype, dela
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     ok, stop, acts, counts = open(tmp_path / "r.txt").read().split(" ", 3)
     assert ok == "True" and stop == "converged", (ok, stop, acts, counts)
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+
+        import paper_2110_10762_b200 as pb
+        from paper_2110_10762_b200 import distributed as D
+        from paper_2110_10762_b200.inputs import sine_u0_1d
+        torch.cuda.set_device(0)
+        n, p_local, T = 4096, 4, 1.0
+        p = p_local * world
+        ivp = pb.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, T)
+        fine = pb.backward_euler_propagator(ivp, T / p, 20)
+        coarse = pb.backward_euler_propagator(ivp, T / p, 1)
+        u0 = sine_u0_1d(n, 8, 0)
+        res = D.run_parareal_sharded(coarse, fine, u0, p_local, 1e-9)  # default edge: peer-memory mailbox
+        shards = [None] * world
+        dist.all_gather_object(shards, res["shard"].cpu())
+        if rank == 0:
+            full = torch.cat([shards[0]] + [s[1:] for s in shards[1:]])
+            ref = pb.run_parareal(coarse, fine, u0, p, 1e-9)
+            ok = (res["k_final"] == ref.k_final and res["stop_reason"] == ref.stop_reason
+                  and res["deltas"] == ref.deltas and torch.equal(full, ref.final.tensor.cpu()))
+            with open(os.path.join(out_dir, "s.txt"), "w") as f:
+                f.write(f"{ok} {res['k_final']} {ref.k_final} {res['stop_reason']}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_sharded_sync_mailbox_edge_bitwise(gpu, tmp_path):
+    """The synchronous multi-GPU sweep with its chain edge over peer memory
+    (K7: pint_mailbox_push into the next rank's IPC mailbox, sequence-numbered
+    versions; host poll because both ranks share this GPU) equals the
+    single-process run bitwise: same k, stop reason, deltas and iterate."""
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    for pr in procs:
+        if pr.is_alive():
+            pr.kill()
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+    ok, k, kref, stop = open(tmp_path / "s.txt").read().split()
+    assert ok == "True", (k, kref, stop)
