@@ -85,3 +85,45 @@ def test_eps_stop_is_drained_and_below_eps(tmp_path, world, p):
     # fixed point of the two-slot update up to eps-sized changes
     err = np.max(np.abs(final - seq))
     assert err < 1e3 * eps, err
+
+
+def _edge_worker(rank, world, port, p, n, mode, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from async_mp_doubles import CpuOps, FakeProp, ShmTransport
+
+        from paper_2110_10762_b200.async_mp import run_async_parareal_mp
+        from paper_2110_10762_b200.errors import HorizonExhausted
+        ops = CpuOps(n, steps=400, r_f=2.0) if mode == "nonfinite" else CpuOps(n)
+        prop = FakeProp(n)
+        s = np.arange(1, n + 1) / (n + 1)
+        u0 = np.sin(np.pi * s) + 0.3 * np.sin(3 * np.pi * s) + 0.01 * np.sin(n * np.pi * s / 2)
+        kw = {"max_events": 3} if mode == "horizon" else {}
+        try:
+            run_async_parareal_mp(prop, prop, u0, p, None, lanes=2, transport=ShmTransport(), ops=ops,
+                                  coarse_init_rows=ops.coarse_init_rows, **kw)
+            got = "none"
+        except HorizonExhausted as exc:
+            got = f"horizon {exc.trace.stop_reason}"
+        except ValueError as exc:
+            got = f"value {exc}"
+        with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
+            f.write(got)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["horizon", "nonfinite"])
+def test_every_rank_stops_on_horizon_and_nonfinite(tmp_path, mode):
+    """A rank that exhausts its activation budget, or produces a non-finite
+    state, raises the stop word on every board: every rank ends and raises
+    the reference's exception (HorizonExhausted / ValueError,
+    async_engine.py:362-365, linalg.py:74-75) instead of hanging."""
+    world, p = 2, 8
+    mp.spawn(_edge_worker, args=(world, _free_port(), p, 24, mode, str(tmp_path)), nprocs=world, join=True)
+    got = [open(tmp_path / f"r{r}.txt").read() for r in range(world)]
+    if mode == "horizon":
+        assert all(g == "horizon max_events" for g in got), got
+    else:
+        assert all(g.startswith("value") and "finite" in g for g in got), got
