@@ -40,6 +40,7 @@ N_MODES = 32
 METRIC = "fine-propagator grid-point updates/s"
 UNIT = "GPt-updates/s"
 BYTES_PER_UPDATE = 16  # one fp64 read + one fp64 write per grid-point update
+FP64_INSTR_PER_UPDATE = 184 / 32  # tri1d_batch_kernel SASS per thread-step / points per thread
 
 
 def workload_config(n_gpus: int) -> dict:
@@ -356,8 +357,12 @@ def run_ours(args, rank: int, world: int) -> None:
                              "(ncu DRAM bytes/launch) is ~2 state copies"},
         "compute": {"bound": "fp64 pipe + latency (state is register-resident; HBM is not the limit)",
                     "fp64_pipe_frac_ncu": _ncu_field("fp64_pipe_pct_of_peak", 0.01),
-                    "fp64_peak_tfma_s_measured": 17.95,
-                    "source": "profiles/ncu_fine_kernel.json, scripts/microbench.cu"},
+                    # live: this run's F rate x the kernel's FP64 instructions per update
+                    # (SASS: 144 DFMA + 34 DMUL + 6 DADD per 32-point thread-step)
+                    "fp64_instr_per_update": FP64_INSTR_PER_UPDATE,
+                    "fp64_frac_live": updates_per_step / (ms_fine * 1e-3) * FP64_INSTR_PER_UPDATE / 17.95e12,
+                    "fp64_peak_instr_s_measured": 17.95e12,
+                    "source": "profiles/ncu_fine_kernel.json, profiles/r02_ncu_summary.md, scripts/microbench.cu"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "ms_per_step": ms_e2e,
                 "call": "paper_2110_10762_b200.parareal_iterate(coarse, fine, BlockVector(pinned host iterate), "

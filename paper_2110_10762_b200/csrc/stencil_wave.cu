@@ -14,10 +14,13 @@
 // grid-point update. Zero Dirichlet: values outside the domain are 0 at every
 // level. Arithmetic per point is the same expression everywhere (batch ==
 // single, any tiling).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "pint_internal.cuh"
@@ -31,9 +34,51 @@ constexpr int W2 = BX2 + 2 * SMAX2;      // loaded columns per tile
 constexpr int WT2 = W2 / CPT2;           // threads per CTA (136)
 constexpr int YC2 = 128;                 // output rows per chunk
 
-template <typename T, int S, bool UNROLL, int MINB>
+// TMA input ring of the 2-D wavefront (TMA = true): groups of RB2 input rows
+// of the tile arrive in shared memory by two cp.async.bulk.tensor loads each
+// (272 columns exceed the 256-element box limit: two 136-column boxes), the
+// rows outside the grid zero-filled by the TMA unit (the Dirichlet values),
+// D2<T> groups ahead of the wavefront, one mbarrier per ring slot. The tile
+// origin is x0 = 256 bx - 8 for every pass depth (16-byte aligned inner
+// coordinate, as the unit requires).
+constexpr int RB2 = 8;
+template <typename T>
+constexpr int D2() { return sizeof(T) == 8 ? 2 : 4; }
+
+__device__ __forceinline__ void bar_init2(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait2(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TW2_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TW2_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void tma_rows2(const CUtensorMap *map, uint32_t ring, uint32_t bars, int slot, int x0,
+                                          int y, int b) {
+  const uint32_t bar = bars + 8u * (uint32_t)slot;
+  const uint32_t dst = ring + (uint32_t)(slot * RB2 * W2 * (int)sizeof(T));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"((uint32_t)(RB2 * W2 * sizeof(T)))
+               : "memory");
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst + (uint32_t)(h * RB2 * (W2 / 2) * (int)sizeof(T))),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x0 + h * (W2 / 2)), "r"(y), "r"(b), "r"(bar)
+        : "memory");
+}
+
+template <typename T, int S, bool UNROLL, int MINB, bool TMA>
 __global__ void __launch_bounds__(WT2, MINB)
-fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, T r) {
+fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx, int ny, T r,
+          const __grid_constant__ CUtensorMap tmap) {
   const int tid = threadIdx.x;
   // fp64: the edge columns of every thread in two planes (a thread's first /
   // last column), so a warp's neighbour loads and edge stores are contiguous
@@ -51,7 +96,8 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
       for (int c = 0; c < CPT2; ++c) row[1 + CPT2 * tid + c] = vv[c];
     }
   };
-  const int x0 = blockIdx.x * BX2 - S;  // first loaded column (halo S)
+  constexpr int HL = TMA ? SMAX2 : S;   // left halo (TMA: 16-byte aligned origin)
+  const int x0 = blockIdx.x * BX2 - HL;  // first loaded column
   const int y0 = blockIdx.y * YC2;
   const T *src = in + (int64_t)blockIdx.z * stride;
   T *dst = out + (int64_t)blockIdx.z * stride;
@@ -61,7 +107,7 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   for (int c = 0; c < CPT2; ++c) {
     colin[c] = cx + c >= 0 && cx + c < nx;
     const int lc = CPT2 * tid + c;  // local column
-    colout[c] = colin[c] && lc >= S && lc < S + BX2;
+    colout[c] = colin[c] && lc >= HL && lc < HL + BX2;
   }
   for (int i = tid; i < 2 * S * 2 * (WT2 + 2); i += WT2) (&sm[0][0][0][0])[i] = T(0);
   T cur[S][CPT2], prv[S][CPT2], pp[S][CPT2];
@@ -72,10 +118,27 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
   __syncthreads();
   const T four = T(4);
   const int ys = y0 - S, ye = min(y0 + YC2, ny) - 1 + S;
+  // TMA ring (dynamic shared memory): D2 slots of RB2 rows x W2 columns, stored
+  // as two column halves [h][row][136], then D2 mbarriers
+  extern __shared__ __align__(128) unsigned char ring_raw[];
+  uint32_t ring = 0, bars = 0;
+  if constexpr (TMA) {
+    ring = static_cast<uint32_t>(__cvta_generic_to_shared(ring_raw));
+    bars = ring + (uint32_t)(D2<T>() * RB2 * W2 * (int)sizeof(T));
+    if (tid == 0) {
+      for (int d = 0; d < D2<T>(); ++d) bar_init2(bars + 8u * (uint32_t)d);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int d = 0; d < D2<T>() && ys + d * RB2 <= ye; ++d)
+        tma_rows2<T>(&tmap, ring, bars, d, x0, ys + d * RB2, (int)blockIdx.z);
+  }
   // input rows are prefetched one iteration ahead (the load latency would
   // otherwise sit in front of every row's barrier)
   T pre[CPT2];
-  {
+  if constexpr (!TMA) {
     const bool rowin = ys >= 0 && ys < ny;
 #pragma unroll
     for (int c = 0; c < CPT2; ++c) pre[c] = (rowin && colin[c]) ? __ldg(src + (int64_t)ys * nx + cx + c) : T(0);
@@ -86,9 +149,29 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
     constexpr int par = decltype(par_c)::value;
     constexpr bool EDGE = decltype(edge_c)::value;
     // level 0: the input row yy
+    if constexpr (TMA) {
+      const int rr = yy - ys, g = rr / RB2, slot = g % D2<T>();
+      if (rr % RB2 == 0) bar_wait2(bars + 8u * (uint32_t)slot, (uint32_t)(g / D2<T>()) & 1u);
+      // this thread's two columns: half h = tid / 68 of the slot, row rr % RB2
+      const int h = tid >= WT2 / 2 ? 1 : 0;
+      const uint32_t a = ring + (uint32_t)(((slot * 2 + h) * RB2 + rr % RB2) * (W2 / 2) * (int)sizeof(T) +
+                                           (CPT2 * tid - h * (W2 / 2)) * (int)sizeof(T));
+      if constexpr (sizeof(T) == 8) {
+        double2 v;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+        cur[0][0] = v.x;
+        cur[0][1] = v.y;
+      } else {
+        float2 v;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+        cur[0][0] = v.x;
+        cur[0][1] = v.y;
+      }
+    } else {
 #pragma unroll
-    for (int c = 0; c < CPT2; ++c) cur[0][c] = pre[c];
-    {
+      for (int c = 0; c < CPT2; ++c) cur[0][c] = pre[c];
+    }
+    if constexpr (!TMA) {
       const int yn = yy + 1;
       const bool rowin = yn >= 0 && yn < ny && yn <= ye;
 #pragma unroll
@@ -130,6 +213,14 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
         prv[L][c] = cur[L][c];
       }
     __syncthreads();
+    if constexpr (TMA) {
+      // the last row of a group has been read by every thread: refill its slot
+      const int rr = yy - ys;
+      if (rr % RB2 == RB2 - 1 && tid == 0) {
+        const int g = rr / RB2 + D2<T>();
+        if (ys + g * RB2 <= ye) tma_rows2<T>(&tmap, ring, bars, g % D2<T>(), x0, ys + g * RB2, (int)blockIdx.z);
+      }
+    }
   };
   using P0 = std::integral_constant<int, 0>;
   using P1 = std::integral_constant<int, 1>;
@@ -158,19 +249,52 @@ fe2d_wave(const T *__restrict__ in, T *__restrict__ out, int64_t stride, int nx,
 
 // PINT_FE2D_VARIANT (measurement): 0 = rolled row loop, 1 = six-row steady
 // unroll (no register cap), 2 = six-row unroll capped for 3 CTAs/SM (default:
-// C3 fp64 +7 %, fp32 +10 % over 0, profiles/r01_fe2d_variants.jsonl)
+// C3 fp64 +7 %, fp32 +10 % over 0, profiles/r01_fe2d_variants.jsonl),
+// 3 = variant 2 with the TMA input ring, 4 = TMA ring capped for 2 CTAs/SM
 int fe2d_variant() {
   const char *e = getenv("PINT_FE2D_VARIANT");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 3;  // TMA ring: C3 fp64 848 -> 1025 GPt/s, fp32 1399 -> 1407 (profiles/r02_fe2d_variants.jsonl)
 }
 
-template <typename T, int S, bool UNROLL, int MINB>
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder2() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PINT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) pint_throw(PINT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <typename T, int S, bool UNROLL, int MINB, bool TMA>
 void launch2v(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, T r, cudaStream_t st) {
   const unsigned tx = (unsigned)((nx + BX2 - 1) / BX2), ty = (unsigned)((ny + YC2 - 1) / YC2);
+  const bool tma = TMA && ((uintptr_t)in & 15u) == 0 && (nx * sizeof(T)) % 16 == 0 && (stride * sizeof(T)) % 16 == 0;
   for (int64_t b0 = 0; b0 < nb; b0 += 65535) {
     const unsigned n = (unsigned)std::min<int64_t>(65535, nb - b0);
-    fe2d_wave<T, S, UNROLL, MINB><<<dim3(tx, ty, n), WT2, 0, st>>>(in + b0 * stride, out + b0 * stride, stride, nx,
-                                                                   ny, r);
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    if (tma) {
+      cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)n};
+      cuuint64_t strides[2] = {(cuuint64_t)nx * sizeof(T), (cuuint64_t)stride * sizeof(T)};
+      cuuint32_t box[3] = {(cuuint32_t)(W2 / 2), (cuuint32_t)RB2, 1};
+      cuuint32_t es[3] = {1, 1, 1};
+      const CUresult rc = tensor_map_encoder2()(
+          &map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+          const_cast<T *>(in + b0 * stride), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (rc != CUDA_SUCCESS) pint_throw(PINT_ECUDA, "cuTensorMapEncodeTiled refused the row map");
+      auto kern = fe2d_wave<T, S, UNROLL, MINB, true>;
+      const int smem = D2<T>() * RB2 * W2 * (int)sizeof(T) + 8 * D2<T>();
+      PINT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<dim3(tx, ty, n), WT2, smem, st>>>(in + b0 * stride, out + b0 * stride, stride, nx, ny, r, map);
+    } else {
+      fe2d_wave<T, S, UNROLL, MINB, false><<<dim3(tx, ty, n), WT2, 0, st>>>(in + b0 * stride, out + b0 * stride,
+                                                                            stride, nx, ny, r, map);
+    }
   }
   PINT_CUDA(cudaGetLastError());
 }
@@ -178,9 +302,11 @@ void launch2v(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, T
 template <typename T, int S>
 void launch2(const T *in, T *out, int64_t nb, int64_t stride, int nx, int ny, T r, cudaStream_t st) {
   switch (fe2d_variant()) {
-    case 1: launch2v<T, S, true, 1>(in, out, nb, stride, nx, ny, r, st); break;
-    case 2: launch2v<T, S, true, 3>(in, out, nb, stride, nx, ny, r, st); break;
-    default: launch2v<T, S, false, 1>(in, out, nb, stride, nx, ny, r, st); break;
+    case 1: launch2v<T, S, true, 1, false>(in, out, nb, stride, nx, ny, r, st); break;
+    case 2: launch2v<T, S, true, 3, false>(in, out, nb, stride, nx, ny, r, st); break;
+    case 3: launch2v<T, S, true, 3, true>(in, out, nb, stride, nx, ny, r, st); break;
+    case 4: launch2v<T, S, true, 2, true>(in, out, nb, stride, nx, ny, r, st); break;
+    default: launch2v<T, S, false, 1, false>(in, out, nb, stride, nx, ny, r, st); break;
   }
 }
 

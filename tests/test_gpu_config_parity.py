@@ -159,7 +159,7 @@ def test_explicit_fine_map_bitwise_ragged(gpu, n, ndim, steps, cfl, dtype):
     if ndim == 3:
         variants = list(range(0, 15 if dtype == "float32" else 9))
     if ndim == 2:
-        variants = [0, 1, 2]
+        variants = [0, 1, 2, 3, 4]
     key = "PINT_FE3D_VARIANT" if ndim == 3 else "PINT_FE2D_VARIANT"
     want = None
     try:

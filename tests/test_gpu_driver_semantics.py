@@ -88,3 +88,37 @@ def test_parareal_iterate_is_the_unfrozen_sweep(gpu):
         lam = gpu.parareal_iterate(coarse, fine, lam)
     seq = gpu.sequential_fine_solve(fine, ivp.u0, p).data
     assert np.array_equal(lam.data, seq)
+
+
+def test_parareal_iterate_host_buffers_equal_one_run_parareal_sweep(gpu):
+    """The public host-in/host-out call (the bench's e2e) is bitwise one sweep
+    of run_parareal from the same iterate: at the C2 layout (chunked,
+    pipelined, graph-replayed sweep) and at a 3-D generic-chain layout."""
+    import torch
+    from paper_2110_10762_b200.inputs import sine_u0_1d
+    n, p = 65536, 64
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    fine = gpu.backward_euler_propagator(ivp, 1.0 / p, 50)
+    coarse = gpu.backward_euler_propagator(ivp, 1.0 / p, 1)
+    u0 = sine_u0_1d(n, 32, 0)
+    tr = gpu.run_parareal(coarse, fine, u0, p, 0.0, k_max=1, record_iterates=True)
+    host = torch.from_numpy(tr.iterates[0].data.copy()).pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    for _ in range(2):  # second call replays the captured graph
+        new = gpu.parareal_iterate(coarse, fine, gpu.BlockVector(host, check_finite=False), out=out)
+        assert new.tensor.device.type == "cpu"
+        assert torch.equal(new.tensor, tr.iterates[1].tensor.cpu())
+    # 3-D: the generic chain (pint_correct_chain)
+    m, q = 24, 5
+    h = 1.0 / (m + 1)
+    ivp3 = gpu.heat3d_system(m, t_final=1.0)
+    f3 = gpu.forward_euler_propagator(ivp3, 7 * 0.15 * h * h, 7, dtype="float32")
+    g3 = gpu.backward_euler_propagator(ivp3, 7 * 0.15 * h * h, 1, dtype="float32")
+    u3 = np.random.default_rng(2).standard_normal(m ** 3)
+    t3 = gpu.run_parareal(g3, f3, u3, q, 0.0, k_max=2, record_iterates=True)
+    for k in (0, 1):
+        h3 = torch.from_numpy(t3.iterates[k].data.copy())
+        new = gpu.parareal_iterate(g3, f3, gpu.BlockVector(h3, check_finite=False))
+        # slices frozen in run_parareal (i < k) are recomputed F-only from unchanged
+        # inputs by the unfrozen sweep: the same bits
+        assert torch.equal(new.tensor, t3.iterates[k + 1].tensor.cpu())
