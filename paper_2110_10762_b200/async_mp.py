@@ -80,6 +80,7 @@ class CudaTransport:
         self.device = int(prop.device)
         self._opened = []
         self._owned = []
+        self._exports = {}  # handle -> pointer of this process's own exported workspaces
 
     def _chk(self, rc, what):
         _native.check(rc, self.ctx, what)
@@ -97,11 +98,14 @@ class CudaTransport:
     def export(self, ptr: int) -> bytes:
         buf = (ctypes.c_ubyte * 64)()
         self._chk(self.lib.pint_ipc_export(self.ctx, ctypes.c_void_p(ptr), buf), "pint_ipc_export")
+        self._exports[bytes(buf)] = int(ptr)
         return bytes(buf)
 
     def open(self, handle: bytes, own_ptr: int, own_handle: bytes) -> int:
         if handle == own_handle:  # a process cannot open its own allocation
             return own_ptr
+        if handle in self._exports:  # another workspace of this same process
+            return self._exports[handle]
         buf = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
         p = ctypes.c_void_p()
         self._chk(self.lib.pint_ipc_open(self.ctx, buf, ctypes.byref(p)), "pint_ipc_open")

@@ -198,3 +198,51 @@ def test_two_processes_sharded_sync_mailbox_edge_bitwise(gpu, tmp_path):
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     ok, k, kref, stop = open(tmp_path / "s.txt").read().split()
     assert ok == "True", (k, kref, stop)
+
+
+def test_mailbox_edge_device_wait_in_one_process(gpu):
+    """The sync chain edge with the device-side wait (the multi-GPU mode):
+    rank 0's edge pushes into rank 1's workspace, rank 1's stream waits on the
+    version with pint_mailbox_wait — here both ends in one process on one
+    stream (push before wait in stream order), so nothing waits on another
+    process. Sequence numbers, slot parity and the timeout flag are checked."""
+    from paper_2110_10762_b200.async_mp import CudaTransport
+    from paper_2110_10762_b200.distributed import MailboxEdge
+    u0, fine, coarse = _problem(gpu)
+
+    class OneProcExchange:
+        def __init__(self):
+            self.pending = []
+
+        def all_gather_bytes(self, b):
+            # rank 1's edge is built first, rank 0's second: [rank 0, rank 1] handles
+            self.pending.append(b)
+            return [b, b] if len(self.pending) == 1 else [b, self.pending[0]]
+
+        def all_gather_object(self, obj):
+            return [obj, ("other-host", obj[1])]
+
+    n = 5000
+    like = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ex = OneProcExchange()
+    tp = CudaTransport(fine)
+    recv_edge = MailboxEdge(like, 1, 2, tp, ex, wait="device")      # rank 1 (consumer): allocates first
+    send_edge = MailboxEdge(like, 0, 2, tp, ex, wait="device")      # rank 0 (producer): next = rank 1's ws
+    assert send_edge.peer_next == recv_edge.ws
+    row0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    d0 = torch.empty(1, dtype=torch.float64, device="cuda")
+    for k in range(5):
+        row = torch.arange(n, dtype=torch.float64, device="cuda") * (k + 1)
+        dl = torch.tensor([0.5 * k], dtype=torch.float64, device="cuda")
+        send_edge.send(k, row, dl)
+        recv_edge.recv(k, row0, d0)
+        torch.cuda.synchronize()
+        assert torch.equal(row0, row) and float(d0) == 0.5 * k
+        assert int(recv_edge.ver[0]) == k + 1
+    recv_edge.check()
+    # a version that never comes: the device wait gives up and the flag raises
+    tp.wait_version(recv_edge.ver.data_ptr(), 99, recv_edge.timed_out, torch.cuda.current_stream(), timeout_s=0.05)
+    torch.cuda.synchronize()
+    with pytest.raises(RuntimeError):
+        recv_edge.check()
+    tp.close()
