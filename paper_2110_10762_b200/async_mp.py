@@ -266,6 +266,7 @@ class _Runtime:
         self.R = int(ring)
         self.max_events, self.delay_frac, self.seed = int(max_events), float(delay_frac), int(seed)
         self.record_trace = record_trace
+        self.claim = "lowest"
         esz = torch.empty(0, dtype=self.dtype).element_size()
         self.row_bytes = self.n * esz
         self.slot_bytes = (self.row_bytes + 255) // 256 * 256
@@ -474,10 +475,16 @@ class _Runtime:
                                 time.perf_counter_ns(), ln.index + 65536 * self.rank))
 
         def pick():
+            # lowest slice with something to do first (the pipeline order of the
+            # sweeps; any order is a valid asynchronous schedule); "round-robin"
+            # walks a ticket over the slices instead
             nonlocal ticket
-            for _ in range(nl):
-                li = 1 + ticket % nl
-                ticket += 1
+            for q in range(nl):
+                if self.claim == "round-robin":
+                    li = 1 + ticket % nl
+                    ticket += 1
+                else:
+                    li = 1 + q
                 if busy[li]:
                     continue
                 if stable[li] and consumed[li] == visible(li - 1):
@@ -611,14 +618,17 @@ def device_coarse_init_rows(coarse, u0, first: int, last: int) -> torch.Tensor:
 def run_async_parareal_mp(coarse, fine, u0, p: int, epsilon: float | None = None, *, lanes: int = 2,
                           ring: int = 3, max_events: int = 200_000, delay_frac: float = 0.0, seed: int = 0,
                           record_trace: bool = False, gather: bool = False, group=None, transport=None, ops=None,
-                          exchange=None, coarse_init_rows=None) -> MPAsyncResult:
+                          exchange=None, coarse_init_rows=None, claim: str = "lowest") -> MPAsyncResult:
     """Asynchronous Parareal across processes/GPUs (see the module docstring).
 
     Every rank calls it with the same arguments. Returns this rank's
     ``MPAsyncResult`` (its rows; the gathered ``final`` on rank 0 when
     ``gather``). ``epsilon=None`` stops on exact quiescence. Raises
     ``HorizonExhausted`` when a rank reaches ``max_events`` activations first,
-    ``ValueError`` on non-finite states (async_parareal.py:61-84 semantics)."""
+    ``ValueError`` on non-finite states (async_parareal.py:61-84 semantics).
+    ``claim``: which ready slice a free lane takes — "lowest" (the pipeline
+    order of the sweeps, default) or "round-robin" (a ticket over the slices);
+    both are valid asynchronous schedules with the same reads and stop rule."""
     import torch.distributed as dist
     if epsilon is not None and epsilon <= 0.0:
         raise ValueError(f"epsilon must be positive, got {epsilon}")
@@ -632,8 +642,11 @@ def run_async_parareal_mp(coarse, fine, u0, p: int, epsilon: float | None = None
     transport = transport or CudaTransport(fine)
     ops = ops or GpuOps(coarse, fine)
     coarse_init_rows = coarse_init_rows or device_coarse_init_rows
+    if claim not in ("lowest", "round-robin"):
+        raise ValueError(f"claim must be 'lowest' or 'round-robin', got {claim!r}")
     rt = _Runtime(coarse, fine, u0, p, epsilon, lanes, ring, max_events, delay_frac, seed, record_trace, rank, world,
                   transport, ops, exchange, coarse_init_rows)
+    rt.claim = claim
     exchange.barrier()  # every mailbox and board is initialised before any rank may push or post
     out = rt.run()
     exchange.barrier()  # no rank frees its workspace while a peer may still store into it

@@ -88,7 +88,7 @@ class StreamAsyncResult:
 def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None = None, *, lanes: int = 4,
                                domains: int = 1, ring: int = 3, max_events: int = 200_000,
                                delay_frac: float = 0.0, seed: int = 0,
-                               record_trace: bool = True) -> StreamAsyncResult:
+                               record_trace: bool = True, claim: str = "lowest") -> StreamAsyncResult:
     if p < 1:
         raise ValueError(f"need p >= 1 subintervals, got {p}")
     if epsilon is not None and epsilon <= 0.0:
@@ -99,6 +99,8 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
         raise ValueError(f"need at least one lane per domain, got lanes={lanes}, domains={domains}")
     if ring < 2:
         raise ValueError("the version ring needs at least two slots")
+    if claim not in ("lowest", "round-robin"):
+        raise ValueError(f"claim must be 'lowest' or 'round-robin', got {claim!r}")
     dev = f"cuda:{fine.device}"
     n, dtype = fine.dim, fine.dtype
     R = int(ring)
@@ -270,11 +272,17 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
     mb_readers = {i: [[] for _ in range(R)] for i in mailbox}
 
     def pick(dom: int):
+        # the lowest slice of the domain with something to do first (the
+        # pipeline order of the sweeps), or a round-robin ticket; both are
+        # valid asynchronous schedules with the same reads and stop rule
         lo, hi = parts[dom]
         m = hi - lo + 1
-        for _ in range(m):
-            i = lo + tickets[dom] % m
-            tickets[dom] += 1
+        for q in range(m):
+            if claim == "round-robin":
+                i = lo + tickets[dom] % m
+                tickets[dom] += 1
+            else:
+                i = lo + q
             if busy[i]:
                 continue
             if stable[i] and consumed[i] == visible(i - 1):

@@ -533,17 +533,21 @@ void apply_tile(const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, 
 //         12 = variant 8 with TMA input planes, 13 = variant 3 with TMA, 14 = variant 9 with TMA,
 //         15 = TMA S2 128x48 (NW16 RPT3 CPT4), 16 = TMA S3 64x48 (NW24 RPT2), 17 = TMA S3 64x64 (NW16 RPT4),
 //         18 = TMA S3 64x48 (NW12 RPT4), 19 = TMA S4 64x48 (NW8 RPT6), 20 = TMA S4 64x50 (NW10 RPT5),
-//         21 = TMA S4 64x48 (NW12 RPT4), 22 = TMA S4 64x32 (NW8 RPT4), 23 = TMA S4 64x60 (NW12 RPT5)
+//         21 = TMA S4 64x48 (NW12 RPT4), 22 = TMA S4 64x32 (NW8 RPT4), 23 = TMA S4 64x60 (NW12 RPT5),
+//         24 = TMA S3 64x48 (NW8 RPT6), 25 = TMA S4 64x40 (NW8 RPT5), 26 = TMA S4 64x36 (NW6 RPT6)
 //         (2-CTA/SM caps of the TMA tiles were dropped: ptxas 12.9 crashes on them)
 //   fp64: 1 = S4 64x16, 2 = S3 64x24, 3 = S3 64x20, 4 = S4 64x32 (NW16 RPT2), 5 = S3 64x32 (NW16 RPT2),
 //         6 = S2 64x32 (NW16 RPT2), 7 = S3 64x40 (NW20 RPT2), 8 = variant 5 with TMA input planes,
 //         9 = TMA S3 64x48 (NW16 RPT3), 10 = TMA S2 64x48 (NW16 RPT3), 11 = TMA S3 64x36 (NW12 RPT3),
 //         12 = TMA S3 64x32 (NW8 RPT4), 13 = TMA S3 64x30 (NW10 RPT3), 14 = TMA S2 64x36 (NW12 RPT3),
-//         15 = TMA S3 64x40 (NW8 RPT5), 16 = TMA S4 64x32 (NW8 RPT4), 17 = TMA S3 64x30 (NW6 RPT5)
+//         15 = TMA S3 64x40 (NW8 RPT5), 16 = TMA S4 64x32 (NW8 RPT4), 17 = TMA S3 64x30 (NW6 RPT5),
+//         18 = TMA S3 64x48 (NW8 RPT6), 19 = TMA S3 64x36 (NW6 RPT6), 20 = TMA S2 64x48 (NW8 RPT6)
 // Defaults measured at the C4 shape (profiles/r02_fe3d_variants.jsonl): the
-// TMA input ring, fp32 948 -> 1109 GPt/s (variant 8 -> 12), fp64 457 -> 600
-// (variant 5 -> 8); 512^3 fp32 1178 -> 1272.
-int fe3d_tile_default(int esz) { return esz == 4 ? 12 : 8; }
+// TMA input ring with deep strips and few warps (fewer y-exchange rows per
+// cell), fp32 948 -> 1331 GPt/s (variant 8 -> 19: S4, 8 warps x 6 rows),
+// fp64 457 -> 707 (variant 5 -> 12: S3, 8 warps x 4 rows); 512^3 fp32
+// 1178 -> 1533.
+int fe3d_tile_default(int esz) { return esz == 4 ? 19 : 12; }
 
 template <typename T>
 bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scratch, int64_t nb, int64_t stride,
@@ -573,6 +577,9 @@ bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scr
       case 21: apply_tile<T, 4, 12, 4, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       case 22: apply_tile<T, 4, 8, 4, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       case 23: apply_tile<T, 4, 12, 5, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 24: apply_tile<T, 3, 8, 6, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 25: apply_tile<T, 4, 8, 5, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 26: apply_tile<T, 4, 6, 6, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       default: return false;
     }
   } else {
@@ -594,6 +601,9 @@ bool fe3d_tile_apply(int variant, const pint_op *op, const T *in, T *out, T *scr
       case 15: apply_tile<T, 3, 8, 5, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       case 16: apply_tile<T, 4, 8, 4, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       case 17: apply_tile<T, 3, 6, 5, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 18: apply_tile<T, 3, 8, 6, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 19: apply_tile<T, 3, 6, 6, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
+      case 20: apply_tile<T, 2, 8, 6, 2, 1, true>(op, in, out, scratch, nb, stride, st); return true;
       default: return false;
     }
   }

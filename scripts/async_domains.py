@@ -23,14 +23,18 @@ def main():
     fine = pb.backward_euler_propagator(ivp, 1 / p, 1000)
     coarse = pb.backward_euler_propagator(ivp, 1 / p, 1)
     seq = pb.sequential_fine_solve(fine, u0, p).data
-    for domains in (1, 2, 4, 8):
+    claims = [int(c) for c in os.environ.get("CLAIMS", "0").split(",")]
+    doms = [int(c) for c in os.environ.get("DOMAINS", "1,2,4,8").split(",")]
+    for claim in claims:
+      os.environ["PINT_ASYNC_CLAIM"] = str(claim)
+      for domains in doms:
         for mode in ("eps", "quiescence"):
             e = eps if mode == "eps" else None
             pb.run_async_parareal_device(coarse, fine, u0, p, e, domains=domains)  # warm
             res = pb.run_async_parareal_device(coarse, fine, u0, p, e, domains=domains, record_trace=True)
             audit = pb.audit_device_trace(res.trace_records, p, res.per_component_counts)
             err = float(np.max(np.abs(res.final.data - seq)))
-            print(json.dumps({"domains": domains, "mode": mode, "epsilon": e, "seconds": res.wall_s,
+            print(json.dumps({"claim": claim, "domains": domains, "mode": mode, "epsilon": e, "seconds": res.wall_s,
                               "kappa": res.kappa, "activations": res.activations, "retries": res.retries,
                               "clusters": res.concurrent_clusters, "max_abs_vs_seq_fine": err,
                               "audit_ok": audit["ok"], "max_staleness": audit["max_staleness"],

@@ -157,7 +157,7 @@ def test_explicit_fine_map_bitwise_ragged(gpu, n, ndim, steps, cfl, dtype):
     us = [u, rng.standard_normal(u.size)]
     variants = [None]
     if ndim == 3:
-        variants = list(range(0, 19)) + [21] if dtype == "float32" else list(range(0, 15))
+        variants = list(range(0, 27)) if dtype == "float32" else list(range(0, 21))
     if ndim == 2:
         variants = [0, 1, 2, 3, 4]
     key = "PINT_FE3D_VARIANT" if ndim == 3 else "PINT_FE2D_VARIANT"
