@@ -270,7 +270,7 @@ class SyncEngine:
                     ctypes.c_void_p(self.deltas.data_ptr()), ctypes.c_void_p(self.flag.data_ptr()), st)
             _native.check(rc, _ctx(self.coarse), "pint_sync_sweep")
         else:
-            self._generic_sweep(k, nxt, chain_in)
+            self._generic_sweep(k, nxt, chain_in, hi)
 
     def reduce_delta(self, k: int, stream=None) -> None:
         st = _stream(self.fine) if stream is None else ctypes.c_void_p(stream.cuda_stream)
@@ -556,18 +556,19 @@ class SyncEngine:
         a, b = ch[-1]
         return 2 * len(ch) - 1 + min(d2h_splits, b - a + 1) + 1
 
-    def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False) -> None:
+    def _generic_sweep(self, k: int, nxt: torch.Tensor, chain_in: bool = False, hi: int | None = None) -> None:
         """Coarse chain + correction for coarse operators without a fused
         sweep kernel (2-D/3-D direct or CG coarse): same values, two launches
         per slice (G, then pint_correct_chain: the F-only branch from the
         predecessor's delta, the G(old) cache refreshed in place)."""
         p, prev = self.p, self.prev
+        hi = p if hi is None else int(hi)
         if not chain_in:
             nxt[k - 1].copy_(prev[k - 1])
         # slice k-1 is frozen (delta 0 => F-only for slice k) unless its new value came in on the chain
-        self.deltas[k if chain_in else k - 1:].zero_()
+        self.deltas[k if chain_in else k - 1:hi + 1].zero_()
         g = self._gbuf(nxt)
-        for i in range(k, p + 1):
+        for i in range(k, hi + 1):
             self.coarse.apply_ptr(nxt[i - 1].data_ptr(), g.data_ptr(), 1, self.fine.dim)
             correct_chain_into(self.fine, g[0], self.fv[i], self.gcache[i], prev[i], nxt[i], self.deltas[i - 1:i],
                                self.deltas[i:i + 1], self.flag)
