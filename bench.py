@@ -640,7 +640,7 @@ def multi_gpu_time_to_tolerance(rank: int, world: int) -> dict:
         fine = pb.backward_euler_propagator(ivp, T_FINAL / P_LOCAL, FINE_STEPS)
         coarse = pb.backward_euler_propagator(ivp, T_FINAL / P_LOCAL, 1)
         u0 = sine_u0_1d(N_POINTS, N_MODES, 0)
-        r = dist_rt.run_async_parareal_distributed(coarse, fine, u0, P_LOCAL, 1e-10, gather=False)
+        r = dist_rt.run_async_parareal_distributed(coarse, fine, u0, P_LOCAL, 1e-10, gather=False, max_events=20_000)
         out["c2_async_1d"] = {"seconds": r["wall_s"], "kappa": r["kappa"], "activations": r["activations"],
                               "stop_reason": r["stop_reason"], "slices": P_LOCAL, "n_gpus": world}
     except Exception as exc:
@@ -654,7 +654,7 @@ def multi_gpu_time_to_tolerance(rank: int, world: int) -> dict:
         fine = pb.forward_euler_propagator(ivp, span, steps, dtype="float32")
         coarse = pb.backward_euler_propagator(ivp, span, 1, dtype="float32")
         u0 = _sine_u0_device(shape).to(torch.float32)
-        r = run_async_parareal_mp(coarse, fine, u0, p, cfg["eps"], lanes=2)
+        r = run_async_parareal_mp(coarse, fine, u0, p, cfg["eps"], lanes=2, max_events=20_000, timeout_s=120.0)
         out["c4_async_nd"] = {"seconds": r.wall_s, "kappa": r.kappa, "activations": r.activations,
                               "stop_reason": r.stop_reason, "slices": p, "n_gpus": world}
     except Exception as exc:

@@ -267,6 +267,7 @@ class _Runtime:
         self.max_events, self.delay_frac, self.seed = int(max_events), float(delay_frac), int(seed)
         self.record_trace = record_trace
         self.claim = "lowest"
+        self.timeout_s = None
         esz = torch.empty(0, dtype=self.dtype).element_size()
         self.row_bytes = self.n * esz
         self.slot_bytes = (self.row_bytes + 255) // 256 * 256
@@ -519,6 +520,10 @@ class _Runtime:
             if done and self._consistent(bd) and self._consistent_again(bd):
                 self._post_stop(STOP_CONVERGED)
                 continue
+            if self.timeout_s is not None and stop_code == 0 and time.perf_counter() - t_begin > self.timeout_s:
+                stop_code = STOP_HORIZON  # wall-clock budget spent: stop every rank like a horizon
+                self._post_stop(STOP_HORIZON)
+                continue
             if events >= self.max_events and stop_code == 0:
                 stop_code = STOP_HORIZON
                 self._post_stop(STOP_HORIZON)
@@ -618,7 +623,8 @@ def device_coarse_init_rows(coarse, u0, first: int, last: int) -> torch.Tensor:
 def run_async_parareal_mp(coarse, fine, u0, p: int, epsilon: float | None = None, *, lanes: int = 2,
                           ring: int = 3, max_events: int = 200_000, delay_frac: float = 0.0, seed: int = 0,
                           record_trace: bool = False, gather: bool = False, group=None, transport=None, ops=None,
-                          exchange=None, coarse_init_rows=None, claim: str = "lowest") -> MPAsyncResult:
+                          exchange=None, coarse_init_rows=None, claim: str = "lowest",
+                          timeout_s: float | None = None) -> MPAsyncResult:
     """Asynchronous Parareal across processes/GPUs (see the module docstring).
 
     Every rank calls it with the same arguments. Returns this rank's
@@ -628,7 +634,9 @@ def run_async_parareal_mp(coarse, fine, u0, p: int, epsilon: float | None = None
     ``ValueError`` on non-finite states (async_parareal.py:61-84 semantics).
     ``claim``: which ready slice a free lane takes — "lowest" (the pipeline
     order of the sweeps, default) or "round-robin" (a ticket over the slices);
-    both are valid asynchronous schedules with the same reads and stop rule."""
+    both are valid asynchronous schedules with the same reads and stop rule.
+    ``timeout_s``: a wall-clock budget after which every rank stops as on the
+    activation horizon (``HorizonExhausted``)."""
     import torch.distributed as dist
     if epsilon is not None and epsilon <= 0.0:
         raise ValueError(f"epsilon must be positive, got {epsilon}")
@@ -647,6 +655,7 @@ def run_async_parareal_mp(coarse, fine, u0, p: int, epsilon: float | None = None
     rt = _Runtime(coarse, fine, u0, p, epsilon, lanes, ring, max_events, delay_frac, seed, record_trace, rank, world,
                   transport, ops, exchange, coarse_init_rows)
     rt.claim = claim
+    rt.timeout_s = timeout_s
     exchange.barrier()  # every mailbox and board is initialised before any rank may push or post
     out = rt.run()
     exchange.barrier()  # no rank frees its workspace while a peer may still store into it

@@ -29,10 +29,13 @@ def main():
     coarse = pb.backward_euler_propagator(ivp, span, 1, dtype="float32")
     torch.cuda.reset_peak_memory_stats()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    tr = pb.run_parareal(coarse, fine, u0, p, eps, record_iterates=False)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import ClockSampler
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        tr = pb.run_parareal(coarse, fine, u0, p, eps, record_iterates=False)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
     peak = torch.cuda.max_memory_allocated() / 2**30
     final = tr.final.tensor
     x = torch.tensor(u0, dtype=torch.float32, device="cuda").reshape(1, -1)
@@ -45,7 +48,7 @@ def main():
     print(json.dumps({"config": "C5", "shape": [n, n, n], "slices": p, "fine_steps": steps, "dtype": "float32",
                       "epsilon": eps, "seconds": wall, "k": tr.k_final, "stop": tr.stop_reason,
                       "deltas": tr.deltas, "peak_hbm_gib": peak, "max_abs_vs_seq_fine": err,
-                      "engine": "lean (in place, 2 state copies)"}), flush=True)
+                      "engine": "lean (in place, 2 state copies)", "clocks": clk.summary()}), flush=True)
 
 
 if __name__ == "__main__":
