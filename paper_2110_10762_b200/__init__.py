@@ -70,6 +70,7 @@ from .costmodel import (
     speedup_bound,
     sync_cost,
 )
+from .async_mp import run_async_parareal_mp
 from .linalg import BlockVector
 from .model import (
     PROPAGATOR_RULES,

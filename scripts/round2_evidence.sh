@@ -16,4 +16,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:fe3d
   -o gpurun_out/r2ev_fe3d -f python scripts/profile_nd.py c4_f32 16 3 > gpurun_out/r2ev_ncu_fe3d.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:fe2d_wave -c 1 \
   -o gpurun_out/r2ev_fe2d -f python scripts/profile_nd.py c3_f64 32 8 > gpurun_out/r2ev_ncu_fe2d.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:tri1d_sweep_kernel -c 1 \
+  -o gpurun_out/r2ev_sweep -f python scripts/profile_c2.py sweep > gpurun_out/r2ev_ncu_sweep.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:xform_tc -c 2 \
+  -o gpurun_out/r2ev_xform -f python scripts/profile_coarse.py c4_f32 2 > gpurun_out/r2ev_ncu_xform.log 2>&1
 ls -la gpurun_out | grep r2ev
