@@ -20,4 +20,11 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:tri1
   -o gpurun_out/r2ev_sweep -f python scripts/profile_c2.py sweep > gpurun_out/r2ev_ncu_sweep.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:xform_tc -c 2 \
   -o gpurun_out/r2ev_xform -f python scripts/profile_coarse.py c4_f32 2 > gpurun_out/r2ev_ncu_xform.log 2>&1
+# summaries on the box (the reports are too large to bring back all at once)
+python scripts/ncu_summary.py gpurun_out/r2ev_*.ncu-rep --launches gpurun_out/r2ev_launches.csv \
+  > gpurun_out/r2ev_summary.txt 2>&1
+for r in gpurun_out/r2ev_*.ncu-rep; do
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}_details.csv" 2>/dev/null
+done
+rm -f gpurun_out/r2ev_*.ncu-rep
 ls -la gpurun_out | grep r2ev
