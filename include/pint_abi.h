@@ -385,6 +385,19 @@ int pint_max_reduce(pint_ctx *ctx, const double *deltas_dev, int64_t lo,
 int pint_tri1d_plan_host(const pint_op_desc *desc, int32_t *dims_out,
                          double *fac_out, double *table_out, double *scal_out);
 
+/*
+ * Host-only export of the backward-Euler fast path's chunk factors (the
+ * constant-coefficient twisted chunk solve, csrc/tri1d.cu): *usable_out = 1
+ * when the operator runs on it (every thread regular, no boundary forcing,
+ * strictly diagonally dominant step matrix); fac_out = 11 + 3*(CH/2) doubles
+ * {mu, kap, kapm, al, be, ga, sAB, sB, nlam, CmAB, CmN, g[CH/2],
+ * 1/rho[CH/2], rho[CH/2]}. CH is desc->layout_ch (16) or 32. Used by the CPU tests to
+ * emulate the kernel; replaces nothing in the reference (the reference's
+ * step is a dense LU solve, linalg.py:241-266).
+ */
+int pint_tri1d_ccst_host(const pint_op_desc *desc, int32_t *usable_out,
+                         double *fac_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,6 +108,7 @@ SIGNATURES = {
     "pint_board_post": (c_int, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "pint_board_read": (c_int, [c_void_p, c_void_p, c_i32, c_void_p, c_void_p]),
     "pint_tri1d_plan_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pint_tri1d_ccst_host": (c_int, [ctypes.POINTER(OpDesc), c_void_p, c_void_p]),
 }
 
 _lib = None

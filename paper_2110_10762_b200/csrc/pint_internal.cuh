@@ -61,6 +61,28 @@ struct ChunkFactors {
   double ws[CH];  // w / q: y0 from the pivot-scaled state t = q x   [backward Euler]
 };
 
+// Constant-coefficient twisted chunk solve (backward-Euler fast path, see
+// tri1d.cu): the CH-1 chunk points are eliminated from both ends toward the
+// middle point k with the limit factors of the Toeplitz LU (one multiplier mu
+// for every row), the state is kept scaled by rho_j = lambda^|j-k| so that
+// both sweeps are single FMAs with position-independent coefficients, and the
+// two corner defects of the constant factorisation are folded into the
+// separator terms on the host.
+template <int CH>
+struct CcstFactors {
+  double mu;    // lambda^2: elimination multiplier (scaled variables)
+  double kap;   // 1/c: substitution multiplier
+  double kapm;  // 1/(c (1 - mu)): middle pivot
+  double al, be, ga;  // z_0 = al P + be Q + ga w, z_L = be P + al Q + ga w
+  double sAB, sB, nlam;  // effective boundary value: sAB s_near + sB (s_far - s_near) + nlam z_near
+  double CmAB;  // x_k = CmAB (s_left + s) + CmN (z_0 + z_L) + kapm w
+  double CmN;
+  double g[CH / 2];   // psi_j += g_j sigma' (j < k; mirrored for the lower half)
+  double rs[CH / 2];  // 1 / rho_j
+  double ro[CH / 2];  // rho_j
+};
+inline int ccst_nscalars(int CH) { return 11 + 3 * (CH / 2); }
+
 // Per-thread reduced-system constants, laid out [field][T] in device memory.
 enum Tri1DField {
   TF_MASK = 0,      // 1 if the thread's separator is a real unknown
@@ -90,6 +112,8 @@ struct Tri1DPlan {
   int64_t steps = 1;
   double min_pivot = 0;
   std::vector<double> fac_reg, fac_tail;  // 5*CH each (q,e,h,w,ws)
+  bool ccst = false;                      // constant-coefficient twisted chunk solve usable
+  std::vector<double> ccst_fac;           // CcstFactors<CH> as a flat array (ccst_nscalars)
   std::vector<double> table;              // [nfields][T]
 };
 

@@ -154,6 +154,66 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
     P.fq_last = (P.l_last == CH - 1) ? P.f_last : fl[P.l_last] * P.f_last;
   }
 
+  // Constant-coefficient twisted chunk solve (backward Euler, every thread
+  // regular, no forcing): K = c (I - lam S)(I - lam S^T) away from the chunk
+  // ends, c the larger root of c^2 - D c + E^2 = 0, lam = -E / c. Eliminating
+  // with these limit factors from both chunk ends solves Kt = K_c - delta
+  // (e_0 e_0^T + e_L e_L^T), delta = D - c, exactly; since K_c x = b is
+  // Kt x = b - delta (x_0 e_0 + x_L e_L), the defect acts like a change of the
+  // adjacent separator values (sigma' = sigma - lam x_end) and folds into
+  // data-independent scalars. In the scaled variables chi_j = x_j / lam^|j-k|
+  // both sweeps have position-independent multipliers (mu = lam^2 and 1/c).
+  P.ccst = false;
+  P.ccst_fac.assign(ccst_nscalars(CH), 0.0);
+  if (!cn && m >= 3 && (m & 1) && E != 0.0L && D * D > 4.0L * E * E) {
+    // every factor in closed form in lam (the chunk's Green's function is a
+    // combination of lam^j and lam^-j); 1 - mu = (c - E)(c + E) / c^2 is formed
+    // without cancellation so the factors keep full relative accuracy as
+    // lam -> 1 (large dt / h^2)
+    const int k = (m - 1) / 2, n = m + 1;  // n = 2k + 2: distance between the two separators
+    const ld sd = D >= 0 ? 1.0L : -1.0L;
+    const ld disc = sd * sqrtl((D - 2.0L * E) * (D + 2.0L * E));
+    const ld c = (D + disc) / 2.0L;
+    const ld lam = -E / c;
+    const ld om = ((D - 2.0L * E + disc) / 2.0L) * ((D + 2.0L * E + disc) / 2.0L) / (c * c);  // 1 - mu
+    const ld mu = lam * lam;
+    const ld lk = powl(lam, k);
+    // (not used when the step matrix is E-dominated beyond any grid scale,
+    //  |E| / (|D| - 2|E|) > 100 N^2, i.e. dt >> the slowest mode's time scale:
+    //  the nearly free chunk ends then cost accuracy, measured in
+    //  tests/test_host_logic.py; the exact-pivot path serves those)
+    const bool stiff_ok = fabsl(E) <= 100.0L * (ld)N * (ld)N * (fabsl(D) - 2.0L * fabsl(E));
+    if (fabsl(lk) > 1e-100L && om > 0.0L && stiff_ok) {
+      ld geo = 0.0L, t = 1.0L;  // (1 - lam^(2n)) / (1 - mu)
+      for (int i = 0; i < n; ++i) {
+        geo += t;
+        t *= mu;
+      }
+      const ld ln = powl(lam, n), lk1 = lk * lam;
+      double *f = P.ccst_fac.data();
+      f[0] = (double)mu;
+      f[1] = (double)(1.0L / c);
+      f[2] = (double)(1.0L / (c * om));
+      f[3] = (double)(lk1 / (-E * geo));                       // al
+      f[4] = (double)(-powl(lam, 3 * k + 3) / (-E * geo));     // be
+      f[5] = (double)(lk1 / (-E * (1.0L + ln)));               // ga
+      f[6] = (double)(om / (1.0L + ln));                       // sAB = 1 - lam (vL_0 + vR_0)
+      f[7] = (double)(-ln / geo);                              // sB = -lam vR_0
+      f[8] = (double)(-lam);
+      f[9] = (double)(lk1 / (1.0L + ln));                      // CmAB
+      f[10] = (double)(-lk1 * lam / om);                       // CmN
+      for (int i = 0; i < k; ++i) {
+        f[11 + i] = (double)(-E * powl(lam, 2 * i - k));
+        const ld rho = powl(lam, k - i);
+        f[11 + CH / 2 + i] = (double)(1.0L / rho);
+        f[11 + 2 * (CH / 2) + i] = (double)rho;
+      }
+      bool fin = true;
+      for (int i = 0; i < ccst_nscalars(CH); ++i) fin = fin && std::isfinite(f[i]);
+      P.ccst = fin;
+    }
+  }
+
   auto kclass = [&](int t) -> int { return t < P.tb ? m : (t == P.tb ? ktail : 0); };
   auto inv_of = [&](int t) -> ChunkInv {
     int k = kclass(t);
@@ -513,7 +573,8 @@ static void run_kernel_t(TriKind kind, const pint_op *op, int grid_slices, int c
                          int64_t p, const double *prev, double *next, const double *fv, int64_t k,
                          double *deltas, int32_t *nonfinite, int chain) {
   // GENERAL: a partially filled (tail) thread or boundary forcing; the fast path has neither
-  if (op->plan.tb < op->plan.T || op->plan.f_first != 0.0 || op->plan.f_last != 0.0)
+  // (backward Euler: the fast path is the constant-coefficient twisted chunk solve)
+  if (op->plan.tb < op->plan.T || op->plan.f_first != 0.0 || op->plan.f_last != 0.0 || (!CN && !op->plan.ccst))
     run_kernel<CH, J, CN, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
                                 deltas, nonfinite, chain);
   else
@@ -686,3 +747,22 @@ extern "C" int pint_tri1d_plan_host(const pint_op_desc *d, int32_t *dims_out, do
   }
 }
 
+
+// Host-only export of the backward-Euler fast-path factors (include/pint_abi.h:
+// pint_tri1d_ccst_host).
+extern "C" int pint_tri1d_ccst_host(const pint_op_desc *d, int32_t *usable_out, double *fac_out) {
+  if (!d || !usable_out) return PINT_EARG;
+  try {
+    if (d->ndim != 1 || d->rule != PINT_RULE_BACKWARD_EULER || d->steps < 1 || !(d->span > 0.0)) return PINT_EARG;
+    const int CH = d->layout_ch == 16 ? 16 : 32;
+    const double dt = d->span / (double)d->steps;
+    Tri1DPlan pl = tri1d_plan(d->shape[0], CH, 1.0 - dt * d->a_diag, 0.0 - dt * d->a_off, dt * d->c_first,
+                              dt * d->c_last, false, d->steps);
+    const bool fast = pl.ccst && pl.tb >= pl.T && pl.f_first == 0.0 && pl.f_last == 0.0;
+    *usable_out = fast ? 1 : 0;
+    if (fac_out) memcpy(fac_out, pl.ccst_fac.data(), sizeof(double) * pl.ccst_fac.size());
+    return PINT_OK;
+  } catch (const PintError &e) {
+    return e.code;
+  }
+}

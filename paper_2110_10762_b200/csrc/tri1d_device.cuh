@@ -16,6 +16,7 @@ namespace cg = cooperative_groups;
 template <int CH>
 struct Tri1DParams {
   ChunkFactors<CH> reg, tail;
+  CcstFactors<CH> cc;   // backward-Euler fast path (no tail thread, no forcing)
   const double *table;  // [NF][T]
   int64_t N;
   int64_t steps;
@@ -80,6 +81,66 @@ __device__ __forceinline__ void chunk_back_scaled(double (&x)[CH], const ChunkFa
     const double xr = fma(F.e[j + z], xn, fma(F.h[j + z], s_left, x[j]));
     x[j] = OUT_RAW ? xr : F.q[j + z] * xr;
     xn = xr;
+  }
+}
+
+// ---- constant-coefficient twisted chunk solve (backward-Euler fast path) ----
+// Chunk slots j = 0..m-1 (m = CH-1) hold chi_j = x_j / rho_j between steps.
+template <int CH>
+__device__ __forceinline__ void ccst_scale(double (&x)[CH], const double (&f)[CH / 2]) {
+  constexpr int m = CH - 1, k = (m - 1) / 2;
+#pragma unroll
+  for (int i = 0; i < k; ++i) {
+    x[i] *= f[i];
+    x[m - 1 - i] *= f[i];
+  }
+}
+
+// Elimination from both ends toward the middle (two independent chains) and
+// the two functionals the separator system needs: z0 / zL = first / last
+// component of the chunk solve with zero separators. On return x[j], j != k,
+// holds the eliminated values psi_j and x[k] the zero-separator middle value.
+template <int CH>
+__device__ __forceinline__ void ccst_forward(double (&x)[CH], const CcstFactors<CH> &C, double &z0, double &zL) {
+  constexpr int m = CH - 1, k = (m - 1) / 2;
+  const double mu = C.mu;
+  double P = x[0], Q = x[m - 1];
+#pragma unroll
+  for (int i = 1; i < k; ++i) {
+    x[i] = fma(mu, x[i - 1], x[i]);
+    x[m - 1 - i] = fma(mu, x[m - i], x[m - 1 - i]);
+    P += x[i];
+    Q += x[m - 1 - i];
+  }
+  const double w = fma(mu, x[k - 1] + x[k + 1], x[k]);
+  const double gw = C.ga * w;
+  z0 = fma(C.al, P, fma(C.be, Q, gw));
+  zL = fma(C.be, P, fma(C.al, Q, gw));
+  // the separator-independent part of the middle value
+  x[k] = fma(C.CmN, z0 + zL, C.kapm * w);
+}
+
+// Substitution from the middle outward (two independent chains) once the
+// separators on both sides are known; nlz0 / nlzL = nlam * z0 / zL.
+template <int CH>
+__device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH> &C, double s_left, double s,
+                                          double nlz0, double nlzL, int z) {
+  constexpr int m = CH - 1, k = (m - 1) / 2;
+  const double kap = C.kap;
+  // effective boundary values sigma' = sigma - lam x_end, written so that the
+  // near-cancellation sA + sB (~ 1 - lam) is formed on the host and the
+  // separator difference on the device (both exact to a rounding)
+  const double dS = s - s_left;
+  const double spL = fma(C.sAB, s_left, fma(C.sB, dS, nlz0));
+  const double spR = fma(C.sAB, s, fma(-C.sB, dS, nlzL));
+  x[k] = fma(C.CmAB, s_left + s, x[k]);
+#pragma unroll
+  for (int i = k - 1; i >= 0; --i) {
+    const double g = C.g[i + z];
+    const double tT = fma(g, spL, x[i]);
+    const double tB = fma(g, spR, x[m - 1 - i]);
+    x[i] = fma(kap, tT, x[i + 1]);
+    x[m - 1 - i] = fma(kap, tB, x[m - 2 - i]);
   }
 }
 
@@ -195,6 +256,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
 __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
                                          uint32_t sc, double extra_in, double *extra_out) {
+  constexpr bool CC = !CN && !GENERAL;  // constant-coefficient twisted chunk solve
   const bool regular = !GENERAL || c.t < P.tb;
   const uint32_t tab = opaque(c.tab);
   // A uniform, step-variant zero (step counters stay below 2^31, checked on
@@ -208,6 +270,8 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (CN) {
 #pragma unroll
     for (int j = 0; j < CH; ++j) xo[j] = x[j];
+  } else if (CC) {
+    if (IN_RAW) ccst_scale<CH>(x, P.cc.rs);
   } else if (IN_RAW) {
     if (regular) chunk_scale<CH>(x, P.reg, z);
     else chunk_scale<CH>(x, P.tail, z);
@@ -220,17 +284,24 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
         if (j == P.l_last) x[j] += P.f_last;
     }
   }
-  double y0;
-  if (CN) {
+  double y0, ylast;
+  if (CC) {
+    ccst_forward<CH>(x, P.cc, y0, ylast);
+  } else if (CN) {
     if (regular) y0 = chunk_forward_raw<CH>(x, P.reg, z);
     else y0 = chunk_forward_raw<CH>(x, P.tail, z);
+    ylast = x[CH - 2];
   } else {
     if (regular) y0 = chunk_forward_scaled<CH>(x, P.reg, z);
     else y0 = chunk_forward_scaled<CH>(x, P.tail, z);
+    ylast = x[CH - 2];
   }
   PHASE(1)
-  const double ylast = x[CH - 2];
   const double dsep = x[CH - 1];
+  // (fast path) the corner terms of the effective boundary values, formed
+  // here, off the critical path that follows the exchange
+  const double nlz0 = CC ? P.cc.nlam * y0 : 0.0;
+  const double nlzL = CC ? P.cc.nlam * ylast : 0.0;
   double y0n = shfl_down_d(y0, 1);
   if (c.lane == 31) y0n = 0.0;
   double b = TAB(TF_MASK) * (dsep - P.E * (ylast + y0n));
@@ -287,7 +358,10 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (c.lane == 0) s_left = sl;
   PHASE(5)
   x[CH - 1] = s;
-  if (CN) {
+  if (CC) {
+    ccst_back<CH>(x, P.cc, s_left, s, nlz0, nlzL, z);
+    if (OUT_RAW) ccst_scale<CH>(x, P.cc.ro);
+  } else if (CN) {
     if (regular) chunk_back_raw<CH>(x, P.reg, s_left, z);
     else chunk_back_raw<CH>(x, P.tail, s_left, z);
   } else {
@@ -408,6 +482,17 @@ static Tri1DParams<CH> make_params(const pint_op *op) {
     P.tail.w[j] = pl.fac_tail[3 * CH + j];
     P.reg.ws[j] = pl.fac_reg[4 * CH + j];
     P.tail.ws[j] = pl.fac_tail[4 * CH + j];
+  }
+  if (pl.ccst) {
+    const double *f = pl.ccst_fac.data();
+    P.cc.mu = f[0]; P.cc.kap = f[1]; P.cc.kapm = f[2];
+    P.cc.al = f[3]; P.cc.be = f[4]; P.cc.ga = f[5];
+    P.cc.sAB = f[6]; P.cc.sB = f[7]; P.cc.nlam = f[8]; P.cc.CmAB = f[9]; P.cc.CmN = f[10];
+    for (int i = 0; i < CH / 2; ++i) {
+      P.cc.g[i] = f[11 + i];
+      P.cc.rs[i] = f[11 + CH / 2 + i];
+      P.cc.ro[i] = f[11 + 2 * (CH / 2) + i];
+    }
   }
   P.table = op->d_table;
   P.N = pl.N;

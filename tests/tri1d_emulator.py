@@ -32,8 +32,16 @@ def export_plan(n, a_d, a_o, c_first, c_last, span, steps, rule="backward-euler"
     rc = lib.pint_tri1d_plan_host(ctypes.byref(d), dims, fac.ctypes.data_as(ctypes.c_void_p),
                                   tab.ctypes.data_as(ctypes.c_void_p), scal.ctypes.data_as(ctypes.c_void_p))
     assert rc == 0
+    ccst, ccfac = False, None
+    if rule == "backward-euler":
+        usable = ctypes.c_int32(0)
+        ccfac = np.zeros(11 + 3 * (CH // 2))
+        rc = lib.pint_tri1d_ccst_host(ctypes.byref(d), ctypes.byref(usable), ccfac.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        ccst = bool(usable.value)
     return dict(CH=CH, T=T, nW=nW, J=J, tb=tb, NF=NF, fac=fac.reshape(2, 5, CH), tab=tab.reshape(NF, T),
-                D=scal[0], E=scal[1], f_first=scal[2], f_last=scal[3], N=n, cn=(rule == "trapezoidal"))
+                D=scal[0], E=scal[1], f_first=scal[2], f_last=scal[3], N=n, cn=(rule == "trapezoidal"),
+                ccst=ccst, ccfac=ccfac)
 
 
 def _fma(a, b, c):
@@ -66,12 +74,35 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     xo = x.copy()
     tab = P["tab"]
     cn = P["cn"]
-    if not cn:
+    cc = P.get("ccst", False) and not cn
+    if cc:
+        # fast path (tri1d_device.cuh: ccst_scale / ccst_forward / ccst_back)
+        m, k, h2 = CH - 1, (CH - 2) // 2, CH // 2
+        f = P["ccfac"]
+        mu, kap, kapm, al, be, ga, sAB, sB, nlam, CmAB, CmN = f[:11]
+        g, rs, ro = f[11:11 + h2], f[11 + h2:11 + 2 * h2], f[11 + 2 * h2:11 + 3 * h2]
+        for i in range(k):
+            x[:, i] = x[:, i] * rs[i]
+            x[:, m - 1 - i] = x[:, m - 1 - i] * rs[i]
+    elif not cn:
         x[:, :CH - 1] = q[:, :CH - 1] * x[:, :CH - 1]
     if P["f_first"] != 0.0 or P["f_last"] != 0.0:
         raise NotImplementedError("emulator covers the zero-forcing case")
     d = x.copy()
-    if cn:
+    if cc:
+        Ps, Qs = d[:, 0].copy(), d[:, m - 1].copy()
+        for i in range(1, k):
+            d[:, i] = _fma(mu, d[:, i - 1], d[:, i])
+            d[:, m - 1 - i] = _fma(mu, d[:, m - i], d[:, m - 1 - i])
+            Ps = Ps + d[:, i]
+            Qs = Qs + d[:, m - 1 - i]
+        wmid = _fma(mu, d[:, k - 1] + d[:, k + 1], d[:, k])
+        gw = ga * wmid
+        y0 = _fma(al, Ps, _fma(be, Qs, gw))
+        zL = _fma(be, Ps, _fma(al, Qs, gw))
+        d[:, k] = _fma(CmN, y0 + zL, kapm * wmid)
+        d[:, CH - 2] = d[:, CH - 2]  # (ylast below is zL)
+    elif cn:
         y0 = w[:, 0] * d[:, 0]
         d[:, 0] = q[:, 0] * d[:, 0]
         for j in range(1, CH - 1):
@@ -82,7 +113,7 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
         for j in range(1, CH - 1):
             y0 = _fma(ws[:, j], d[:, j], y0)
             d[:, j] = _fma(e[:, j], d[:, j - 1], d[:, j])
-    ylast = d[:, CH - 2]
+    ylast = zL if cc else d[:, CH - 2]
     dsep = d[:, CH - 1]
     lane = np.arange(T) % 32
     y0n = _shfl_down(y0, 1)
@@ -117,6 +148,21 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     s_left[lane == 0] = sl[lane == 0]
     out = d.copy()
     out[:, CH - 1] = s
+    if cc:
+        nlz0, nlzL = nlam * y0, nlam * zL
+        dS = s - s_left
+        spL = _fma(sAB, s_left, _fma(sB, dS, nlz0))
+        spR = _fma(sAB, s, _fma(-sB, dS, nlzL))
+        out[:, k] = _fma(CmAB, s_left + s, d[:, k])
+        for i in range(k - 1, -1, -1):
+            tT = _fma(g[i], spL, d[:, i])
+            tB = _fma(g[i], spR, d[:, m - 1 - i])
+            out[:, i] = _fma(kap, tT, out[:, i + 1])
+            out[:, m - 1 - i] = _fma(kap, tB, out[:, m - 2 - i])
+        for i in range(k):
+            out[:, i] = out[:, i] * ro[i]
+            out[:, m - 1 - i] = out[:, m - 1 - i] * ro[i]
+        return out.reshape(-1)[:N]
     xn = s.copy()
     for j in range(CH - 2, -1, -1):
         xr = _fma(e[:, j], xn, _fma(h[:, j], s_left, d[:, j]))
