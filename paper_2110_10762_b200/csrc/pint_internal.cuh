@@ -93,9 +93,12 @@ enum Tri1DField {
   TF_V1 = 13,       // level-1 right spike (coefficient of S_W)
   TF_CP = 14,       // lane 31: coupling of S_W to lane 30
   TF_R2 = 15,       // 2*J fields: rows W-1 / W of R2^{-1}, columns lane + 32 j
-  // then 2*J fields: cZ / cQ for V = lane + 32 j
+  // then TF_HQ / TF_HZ: coefficients of this warp's lane-0 values (y1_0, y0_0)
+  //      in the level-2 right-hand side of the previous warp
 };
-inline int tri1d_nfields(int J) { return 15 + 4 * J; }
+#define TF_HQ(J) (15 + 2 * (J))
+#define TF_HZ(J) (16 + 2 * (J))
+inline int tri1d_nfields(int J) { return 17 + 2 * J; }
 
 struct Tri1DPlan {
   int64_t N = 0;
@@ -105,6 +108,7 @@ struct Tri1DPlan {
   int J = 1;    // ceil(nW / 32)
   int tb = 0;   // number of regular threads
   double D = 1, E = 0;
+  double hq = 0;  // regular separator coupling Ro (fast path's uniform TF_HQ)
   double f_first = 0, f_last = 0;  // per-step rhs forcing at point 0 / N-1 (raw)
   double fq_first = 0, fq_last = 0;  // the same in the pivot-scaled state
   int t_last = 0, l_last = 0;      // thread / slot of point N-1

@@ -234,6 +234,7 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
     if (real(t + 1)) Ro[t] = -E * E * ireg.i0L;
   }
   auto RoAt = [&](int t) -> ld { return (t < 0 || t >= T) ? 0.0L : Ro[t]; };
+  P.hq = (double)(-E * E * ireg.i0L);
 
   const int NF = tri1d_nfields(J);
   P.table.assign((size_t)NF * T, 0.0);
@@ -268,7 +269,7 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       for (int l = 0; l < 31; ++l) { pa[l] = na[l]; pb[l] = nb[l]; pc[l] = nc[l]; }
     }
     for (int l = 0; l < 31; ++l) TBL(TF_PCR_INV, t0 + l) = (double)(1.0L / pb[l]);
-    TBL(TF_PCR_INV, t0 + 31) = 1.0;
+    TBL(TF_PCR_INV, t0 + 31) = 0.0;  // lane 31's value is the level-2 unknown: s = 0 + 0 sl + 1 sr
     // spikes: R_CC^{-1} e_0 and e_30
     ld z0[31], z30[31];
     for (int l = 0; l < 31; ++l) { z0[l] = 0; z30[l] = 0; }
@@ -285,7 +286,20 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       TBL(TF_W1, t0 + l) = (double)w1[W][l];
       TBL(TF_V1, t0 + l) = (double)v1[W][l];
     }
+    TBL(TF_W1, t0 + 31) = 0.0;
+    TBL(TF_V1, t0 + 31) = 1.0;
     TBL(TF_CP, t0 + 31) = (double)RoAt(t0 + 30);
+    // level-2 right-hand side of warp W - 1: B = gP_{W-1} - h_W, h_W = cq y1_0 + cz y0_0
+    // with the coefficients of column W - 1 (lane 31 of the previous warp)
+    {
+      const int t31p = t0 - 1;
+      const double cz = (W >= 1 && real(t31p)) ? (double)E : 0.0;
+      const double cq = (W >= 1) ? (double)RoAt(t31p) : 0.0;
+      for (int l = 0; l < 32; ++l) {
+        TBL(TF_HQ(J), t0 + l) = cq;
+        TBL(TF_HZ(J), t0 + l) = cz;
+      }
+    }
     for (int l = 0; l < 32; ++l) TBL(TF_MASK, t0 + l) = real(t0 + l) ? 1.0 : 0.0;
   }
 
@@ -308,18 +322,13 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
     const int W = t / 32, lane = t % 32;
     for (int j = 0; j < J; ++j) {
       const int V = lane + 32 * j;
-      double prevrow = 0.0, currow = 0.0, cz = 0.0, cq = 0.0;
+      double prevrow = 0.0, currow = 0.0;
       if (V < nW) {
         if (W >= 1) prevrow = (double)R2inv[(size_t)(W - 1) * nW + V];
         currow = (double)R2inv[(size_t)W * nW + V];
-        const int t31 = 32 * V + 31;
-        cz = real(t31) ? (double)E : 0.0;
-        cq = (double)RoAt(t31);
       }
       TBL(TF_R2 + j, t) = prevrow;
       TBL(TF_R2 + J + j, t) = currow;
-      TBL(TF_R2 + 2 * J + j, t) = cz;
-      TBL(TF_R2 + 3 * J + j, t) = cq;
     }
   }
   return P;
@@ -398,7 +407,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   // 32*CH-point segment into whichever row owns it), and writes the new
   // iterate and G(new) back the same way after the correction.
   const uint32_t RS = (uint32_t)(3 * CH + 2) * 8u;  // row stride in bytes
-  const uint32_t row = smem_u32(smem + (15 + 4 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
+  const uint32_t row = smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
   const uint32_t wrow0 = row - (uint32_t)c.lane * RS;  // lane 0's row
   const int64_t wbase = (int64_t)(c.t - c.lane) * CH;  // warp segment start (points)
   const bool even = (N & 1) == 0;
@@ -494,10 +503,10 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   if (nanacc != nanacc) bad = true;
   // final reduction for slice p through one more gather round
   {
-    const uint32_t gb = gather_exchange<4>(c, sc, 0.0, 0.0, 0.0, dpart);
+    const uint32_t gb = gather_exchange<3>(c, sc, 0.0, 0.0, dpart);
     const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
     double ex = 0.0;
-    for (int V = c.lane; V < c.nW; V += 32) ex = fmax(ex, lds(gb + 3u * stride8 + (uint32_t)V * 8u));
+    for (int V = c.lane; V < c.nW; V += 32) ex = fmax(ex, lds(gb + 2u * stride8 + (uint32_t)V * 8u));
     ex = warp_max(ex);
     if (rank == 0 && threadIdx.x == 0) deltas[p] = ex;
   }
@@ -574,7 +583,9 @@ static void run_kernel_t(TriKind kind, const pint_op *op, int grid_slices, int c
                          double *deltas, int32_t *nonfinite, int chain) {
   // GENERAL: a partially filled (tail) thread or boundary forcing; the fast path has neither
   // (backward Euler: the fast path is the constant-coefficient twisted chunk solve)
-  if (op->plan.tb < op->plan.T || op->plan.f_first != 0.0 || op->plan.f_last != 0.0 || (!CN && !op->plan.ccst))
+  // (and every separator is a real unknown: N a multiple of CH)
+  if (op->plan.tb < op->plan.T || op->plan.N % CH != 0 || op->plan.f_first != 0.0 || op->plan.f_last != 0.0 ||
+      (!CN && !op->plan.ccst))
     run_kernel<CH, J, CN, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
                                 deltas, nonfinite, chain);
   else
@@ -758,7 +769,7 @@ extern "C" int pint_tri1d_ccst_host(const pint_op_desc *d, int32_t *usable_out, 
     const double dt = d->span / (double)d->steps;
     Tri1DPlan pl = tri1d_plan(d->shape[0], CH, 1.0 - dt * d->a_diag, 0.0 - dt * d->a_off, dt * d->c_first,
                               dt * d->c_last, false, d->steps);
-    const bool fast = pl.ccst && pl.tb >= pl.T && pl.f_first == 0.0 && pl.f_last == 0.0;
+    const bool fast = pl.ccst && pl.tb >= pl.T && pl.N % CH == 0 && pl.f_first == 0.0 && pl.f_last == 0.0;
     *usable_out = fast ? 1 : 0;
     if (fac_out) memcpy(fac_out, pl.ccst_fac.data(), sizeof(double) * pl.ccst_fac.size());
     return PINT_OK;

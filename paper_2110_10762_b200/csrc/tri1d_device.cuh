@@ -21,6 +21,7 @@ struct Tri1DParams {
   int64_t N;
   int64_t steps;
   double E;
+  double hq;  // fast path: coupling of a level-2 separator to its neighbour lane (= Ro)
   double f_first, f_last;
   int T, nW, tb;
   int t_last, l_last;
@@ -144,6 +145,14 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
   }
 }
 
+// Per-thread PCR multipliers of the first NHOIST rounds, held in registers
+// for all steps of an application (the rest are re-read from shared memory
+// every step: the register file holds the state).
+constexpr int NHOIST = 3;
+struct Hoisted {
+  double a[NHOIST], g[NHOIST];
+};
+
 struct StepCtx {
   uint32_t tab;   // shared address: this thread's table row (NF doubles)
   int TB;
@@ -201,12 +210,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
       :: "r"(bar), "r"(parity) : "memory");
 }
 
-// Publish this warp's level-2 values to every CTA of the cluster and wait for
-// the whole slice's values of step `sc` (double buffered by sc & 1; the
-// mbarrier of each buffer completes one phase per use).
+// Publish this warp's level-2 values (gP, gH and, with NV == 3, the extra
+// reduction value) to every CTA of the cluster and wait for the whole slice's
+// values of step `sc` (double buffered by sc & 1; the mbarrier of each buffer
+// completes one phase per use).
 template <int NV>
-__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double v0, double v1, double v2,
-                                                    double v3) {
+__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double v0, double v1, double v2) {
   const uint32_t par = sc & 1u;
   const uint32_t stride = (uint32_t)(c.nW + 1);
   const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
@@ -217,8 +226,7 @@ __device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t s
     const uint32_t o = (uint32_t)c.Wg * 8u;
     st_async_f64(rgb + o, v0, rbar);
     st_async_f64(rgb + stride * 8u + o, v1, rbar);
-    st_async_f64(rgb + 2u * stride * 8u + o, v2, rbar);
-    if (NV == 4) st_async_f64(rgb + 3u * stride * 8u + o, v3, rbar);
+    if (NV == 3) st_async_f64(rgb + 2u * stride * 8u + o, v2, rbar);
   }
   if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * NV * 8u);
   mbar_wait_parity(bar, (sc >> 1) & 1u);
@@ -255,7 +263,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // a raw result (else scaled for the next step). The separator is always raw.
 template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
 __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
-                                         uint32_t sc, double extra_in, double *extra_out) {
+                                         const Hoisted &H, uint32_t sc, double extra_in, double *extra_out) {
   constexpr bool CC = !CN && !GENERAL;  // constant-coefficient twisted chunk solve
   const bool regular = !GENERAL || c.t < P.tb;
   const uint32_t tab = opaque(c.tab);
@@ -304,23 +312,28 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double nlzL = CC ? P.cc.nlam * ylast : 0.0;
   double y0n = shfl_down_d(y0, 1);
   if (c.lane == 31) y0n = 0.0;
-  double b = TAB(TF_MASK) * (dsep - P.E * (ylast + y0n));
+  double b = dsep - P.E * (ylast + y0n);
+  if (GENERAL) b *= TAB(TF_MASK);  // virtual separators (all real on the fast path)
 #pragma unroll
   for (int r = 0; r < 5; ++r) {
     const int d = 1 << r;
     const double bm = shfl_up_d(b, d);
     const double bp = shfl_down_d(b, d);
-    b = fma(-TAB(TF_PCR_G + r), bp, fma(-TAB(TF_PCR_A + r), bm, b));
+    const double ka = r < NHOIST ? H.a[r < NHOIST ? r : 0] : TAB(TF_PCR_A + r);
+    const double kg = r < NHOIST ? H.g[r < NHOIST ? r : 0] : TAB(TF_PCR_G + r);
+    b = fma(-kg, bp, fma(-ka, bm, b));
   }
   PHASE(2)
-  const double y1 = b * TAB(TF_PCR_INV);
+  const double y1 = b * TAB(TF_PCR_INV);  // lane 31: 0 (its value is the level-2 unknown)
   const double y1_30 = shfl_d(y1, 30);
   const double pw = fma(-TAB(TF_CP), y1_30, b);
   const double gP = shfl_d(pw, 31);
-  const double gQ = shfl_d(y1, 0);
-  const double gZ = shfl_d(y0, 0);
+  // what the previous warp's level-2 row needs from this warp, combined on the
+  // sender: h = Ro y1_0 + E y0_0 (lane 0's values; coefficients of column W - 1)
+  const double h0 = GENERAL ? fma(TAB(TF_HQ(J)), y1, TAB(TF_HZ(J)) * y0) : fma(P.hq, y1, P.E * y0);
+  const double gH = shfl_d(h0, 0);
   PHASE(3)
-  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 4 : 3>(c, sc, gP, gQ, gZ, extra_in));
+  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 3 : 2>(c, sc, gP, gH, extra_in));
   PHASE(4)
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
@@ -330,9 +343,8 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     double B = 0.0;
     if (V < c.nW) {
       const uint32_t o = (uint32_t)V * 8u;
-      B = fma(-TAB(TF_R2 + 3 * J + j), lds_free(gb + stride8 + o + 8u),
-              fma(-TAB(TF_R2 + 2 * J + j), lds_free(gb + 2u * stride8 + o + 8u), lds_free(gb + o)));
-      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 3u * stride8 + o));
+      B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
+      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 2u * stride8 + o));
     }
     sl = fma(TAB(TF_R2 + j), B, sl);
     sr = fma(TAB(TF_R2 + J + j), B, sr);
@@ -352,8 +364,8 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     for (int o = 16; o >= 1; o >>= 1) ex = fmax(ex, __shfl_xor_sync(FULLMASK, ex, o));
   }
   if (WITH_EXTRA) *extra_out = ex;
-  double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
-  if (c.lane == 31) s = sr;
+  // the tables of lane 31 (W1 = 0, V1 = 1, y1 = 0) make its value sr
+  const double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
   double s_left = shfl_up_d(s, 1);
   if (c.lane == 0) s_left = sl;
   PHASE(5)
@@ -387,7 +399,7 @@ __device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *s
   c.t = rank * c.TB + threadIdx.x;
   c.lane = threadIdx.x & 31;
   c.Wg = c.t >> 5;
-  const int NF = 15 + 4 * J;  // odd: the per-thread rows are bank-conflict free
+  const int NF = 17 + 2 * J;  // odd: the per-thread rows are bank-conflict free
   double *tab = smem;
   for (int f = 0; f < NF; ++f) tab[threadIdx.x * NF + f] = P.table[(size_t)f * P.T + c.t];
   c.tab = smem_u32(tab + threadIdx.x * NF);
@@ -412,17 +424,24 @@ __device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *s
 template <int CH, int J, bool CN, bool GENERAL>
 __device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
                                           uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
+  Hoisted H;
+#pragma unroll
+  for (int r = 0; r < NHOIST; ++r) {
+    H.a[r] = lds(c.tab + (uint32_t)(TF_PCR_A + r) * 8u);
+    H.g[r] = lds(c.tab + (uint32_t)(TF_PCR_G + r) * 8u);
+  }
   if (S == 1) {
-    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, sc, extra_in, extra_out);
-    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, sc, 0.0, nullptr);
+    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, H, sc, extra_in, extra_out);
+    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, H, sc, 0.0, nullptr);
     ++sc;
     return;
   }
-  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, sc, extra_in, extra_out);
-  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, sc, 0.0, nullptr);
+  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, H, sc, extra_in, extra_out);
+  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, H, sc, 0.0, nullptr);
   ++sc;
-  for (int64_t s = 1; s < S - 1; ++s, ++sc) tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, sc, 0.0, nullptr);
-  tri_step<CH, J, CN, GENERAL, false, true, false>(x, P, c, sc, 0.0, nullptr);
+  for (int64_t s = 1; s < S - 1; ++s, ++sc)
+    tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, H, sc, 0.0, nullptr);
+  tri_step<CH, J, CN, GENERAL, false, true, false>(x, P, c, H, sc, 0.0, nullptr);
   ++sc;
 }
 
@@ -498,6 +517,7 @@ static Tri1DParams<CH> make_params(const pint_op *op) {
   P.N = pl.N;
   P.steps = pl.steps;
   P.E = pl.E;
+  P.hq = pl.hq;
   P.f_first = pl.cn ? pl.f_first : pl.fq_first;
   P.f_last = pl.cn ? pl.f_last : pl.fq_last;
   P.T = pl.T;

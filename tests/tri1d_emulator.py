@@ -128,16 +128,17 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     y1w = y1.reshape(nW, 32)
     bw = b.reshape(nW, 32)
     pw = _fma(-tab[14].reshape(nW, 32)[:, 31], y1w[:, 30], bw[:, 31])
-    Q = np.append(y1w[:, 0], 0.0)
-    Z = np.append(y0.reshape(nW, 32)[:, 0], 0.0)
+    # sender-side combination h_W = cq y1_0 + cz y0_0 (coefficients of column W - 1)
+    hq = tab[15 + 2 * J].reshape(nW, 32)[:, 0]
+    hz = tab[16 + 2 * J].reshape(nW, 32)[:, 0]
+    Hh = np.append(_fma(hq, y1w[:, 0], hz * y0.reshape(nW, 32)[:, 0]), 0.0)
     sl = np.zeros(T)
     sr = np.zeros(T)
     for j in range(J):
         V = lane + 32 * j
         ok = V < nW
         Vc = np.minimum(V, nW - 1)
-        B = np.where(ok, _fma(-tab[15 + 3 * J + j], Q[np.minimum(V + 1, nW)],
-                              _fma(-tab[15 + 2 * J + j], Z[np.minimum(V + 1, nW)], pw[Vc])), 0.0)
+        B = np.where(ok, pw[Vc] - Hh[np.minimum(V + 1, nW)], 0.0)
         sl = sl + tab[15 + j] * B
         sr = sr + tab[15 + J + j] * B
     sl = sl.reshape(nW, 32).sum(axis=1).repeat(32)
