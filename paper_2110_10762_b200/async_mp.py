@@ -498,10 +498,13 @@ class _Runtime:
 
         while True:
             progressed = False
-            for ln in self.lanes:
-                if ln.job is not None and ln.job[4].query():
-                    finish(ln)
-                    progressed = True
+            # retire in dispatch order so a consumer's record follows its
+            # producer's (see async_streams: the audit replays record order)
+            ready = [ln for ln in self.lanes if ln.job is not None and ln.job[4].query()]
+            ready.sort(key=lambda ln: ln.job[3])
+            for ln in ready:
+                finish(ln)
+                progressed = True
             if nonfinite and stop_code == 0:
                 stop_code = STOP_NONFINITE
                 self._post_stop(STOP_NONFINITE)

@@ -293,10 +293,16 @@ def run_async_parareal_streams(coarse, fine, u0, p: int, epsilon: float | None =
 
     while True:
         progressed = False
-        for ln in all_lanes:
-            if ln.job is not None and ln.job[4].query():
-                finish(ln)
-                progressed = True
+        # Completed activations are retired in dispatch order: a consumer is only
+        # dispatched after its producer's publish event completed (visible()
+        # polls the events), so its record must follow the producer's even when
+        # both are found complete in the same pass (the trace audit replays the
+        # records as the publish order).
+        ready = [ln for ln in all_lanes if ln.job is not None and ln.job[4].query()]
+        ready.sort(key=lambda ln: ln.job[3])
+        for ln in ready:
+            finish(ln)
+            progressed = True
         if done():
             stop_reason = "converged"
             break

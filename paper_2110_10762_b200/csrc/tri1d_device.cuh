@@ -148,7 +148,7 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
 // Per-thread PCR multipliers of the first NHOIST rounds, held in registers
 // for all steps of an application (the rest are re-read from shared memory
 // every step: the register file holds the state).
-constexpr int NHOIST = 3;
+constexpr int NHOIST = 4;
 struct Hoisted {
   double a[NHOIST], g[NHOIST];
 };
@@ -210,25 +210,26 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
       :: "r"(bar), "r"(parity) : "memory");
 }
 
-// Publish this warp's level-2 values (gP, gH and, with NV == 3, the extra
-// reduction value) to every CTA of the cluster and wait for the whole slice's
-// values of step `sc` (double buffered by sc & 1; the mbarrier of each buffer
-// completes one phase per use).
-template <int NV>
-__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double v0, double v1, double v2) {
+// Publish this warp's level-2 values to every CTA of the cluster and wait for
+// the whole slice's values of step `sc` (double buffered by sc & 1; the
+// mbarrier of each buffer completes one phase per use). vPH: lanes 0..15 carry
+// gP (row 0), lanes 16..31 gH (row 1); lane & 15 = target CTA. With EXTRA the
+// warp-uniform vX goes to row 2 (a max-reduction riding on the exchange).
+template <bool EXTRA>
+__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double vPH, double vX) {
   const uint32_t par = sc & 1u;
   const uint32_t stride = (uint32_t)(c.nW + 1);
   const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
   const uint32_t bar = c.mbar + par * 8u;
-  if (c.lane < c.CL) {
-    const uint32_t rgb = mapa(gb, (uint32_t)c.lane);
-    const uint32_t rbar = mapa(bar, (uint32_t)c.lane);
+  const int tgt = c.lane & 15;
+  if (tgt < c.CL) {
+    const uint32_t rgb = mapa(gb, (uint32_t)tgt);
+    const uint32_t rbar = mapa(bar, (uint32_t)tgt);
     const uint32_t o = (uint32_t)c.Wg * 8u;
-    st_async_f64(rgb + o, v0, rbar);
-    st_async_f64(rgb + stride * 8u + o, v1, rbar);
-    if (NV == 3) st_async_f64(rgb + 2u * stride * 8u + o, v2, rbar);
+    st_async_f64(rgb + (c.lane < 16 ? 0u : stride * 8u) + o, vPH, rbar);
+    if (EXTRA && c.lane < 16) st_async_f64(rgb + 2u * stride * 8u + o, vX, rbar);
   }
-  if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * NV * 8u);
+  if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * (EXTRA ? 3u : 2u) * 8u);
   mbar_wait_parity(bar, (sc >> 1) & 1u);
   return gb;
 }
@@ -327,13 +328,14 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double y1 = b * TAB(TF_PCR_INV);  // lane 31: 0 (its value is the level-2 unknown)
   const double y1_30 = shfl_d(y1, 30);
   const double pw = fma(-TAB(TF_CP), y1_30, b);
-  const double gP = shfl_d(pw, 31);
   // what the previous warp's level-2 row needs from this warp, combined on the
   // sender: h = Ro y1_0 + E y0_0 (lane 0's values; coefficients of column W - 1)
   const double h0 = GENERAL ? fma(TAB(TF_HQ(J)), y1, TAB(TF_HZ(J)) * y0) : fma(P.hq, y1, P.E * y0);
-  const double gH = shfl_d(h0, 0);
+  // one shuffle fetches both published values: lanes 0..15 take gP from lane
+  // 31, lanes 16..31 take gH from lane 0
+  const double gPH = shfl_d(c.lane == 31 ? pw : h0, c.lane < 16 ? 31 : 0);
   PHASE(3)
-  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA ? 3 : 2>(c, sc, gP, gH, extra_in));
+  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA>(c, sc, gPH, extra_in));
   PHASE(4)
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
@@ -356,8 +358,10 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     keep += __shfl_xor_sync(FULLMASK, lo ? sr : sl, 16);
 #pragma unroll
     for (int o = 8; o >= 1; o >>= 1) keep += __shfl_xor_sync(FULLMASK, keep, o);
-    sl = __shfl_sync(FULLMASK, keep, 0);
-    sr = __shfl_sync(FULLMASK, keep, 16);
+    // every lane of the lower half now holds sl, of the upper half sr
+    const double other = __shfl_xor_sync(FULLMASK, keep, 16);
+    sl = lo ? keep : other;
+    sr = lo ? other : keep;
   }
   if (WITH_EXTRA) {
 #pragma unroll
