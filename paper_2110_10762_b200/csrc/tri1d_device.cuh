@@ -145,12 +145,18 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
   }
 }
 
-// Per-thread PCR multipliers of the first NHOIST rounds, held in registers
+// Per-thread PCR multipliers of the first rounds, held in registers
 // for all steps of an application (the rest are re-read from shared memory
 // every step: the register file holds the state).
-constexpr int NHOIST = 4;
+// (four rounds on the fast path - all five measured no faster at 127 registers;
+// none where the general path.s extra live values
+// would otherwise spill under the two-CTAs-per-SM register cap)
+template <bool GENERAL, bool CN>
+struct HoistCount {
+  static constexpr int value = GENERAL ? 0 : (CN ? 2 : 4);
+};
 struct Hoisted {
-  double a[NHOIST], g[NHOIST];
+  double a[5], g[5];
 };
 
 struct StepCtx {
@@ -320,8 +326,9 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
     const int d = 1 << r;
     const double bm = shfl_up_d(b, d);
     const double bp = shfl_down_d(b, d);
-    const double ka = r < NHOIST ? H.a[r < NHOIST ? r : 0] : TAB(TF_PCR_A + r);
-    const double kg = r < NHOIST ? H.g[r < NHOIST ? r : 0] : TAB(TF_PCR_G + r);
+    constexpr int NH = HoistCount<GENERAL, CN>::value;
+    const double ka = r < NH ? H.a[r] : TAB(TF_PCR_A + r);
+    const double kg = r < NH ? H.g[r] : TAB(TF_PCR_G + r);
     b = fma(-kg, bp, fma(-ka, bm, b));
   }
   PHASE(2)
@@ -430,7 +437,7 @@ __device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH>
                                           uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
   Hoisted H;
 #pragma unroll
-  for (int r = 0; r < NHOIST; ++r) {
+  for (int r = 0; r < HoistCount<GENERAL, CN>::value; ++r) {
     H.a[r] = lds(c.tab + (uint32_t)(TF_PCR_A + r) * 8u);
     H.g[r] = lds(c.tab + (uint32_t)(TF_PCR_G + r) * 8u);
   }
