@@ -149,7 +149,7 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
 // for all steps of an application (the rest are re-read from shared memory
 // every step: the register file holds the state).
 // (four rounds on the fast path - all five measured no faster at 127 registers;
-// none where the general path.s extra live values
+// none where the general path's extra live values
 // would otherwise spill under the two-CTAs-per-SM register cap)
 template <bool GENERAL, bool CN>
 struct HoistCount {
