@@ -144,6 +144,8 @@ typedef struct pint_op_info {
   double min_pivot;
   int32_t batch_wave_slices;   /* 1-D: slices apply_batch keeps resident at once (one wave); 0 = unknown */
   int32_t fused_sweep;         /* 1-D: 1 if pint_sync_sweep's fused kernel fits (shared memory), else 0 */
+  int32_t general;             /* 1-D: 1 if the exact-pivot kernels run (tail thread, forcing, no fast path) */
+  int32_t reserved0;
 } pint_op_info;
 
 int pint_abi_version(void);

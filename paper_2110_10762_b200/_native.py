@@ -56,6 +56,7 @@ class OpInfo(ctypes.Structure):
         ("batch_cluster", c_i32), ("sweep_cluster", c_i32),
         ("dt", c_double), ("diag", c_double), ("offdiag", c_double), ("min_pivot", c_double),
         ("batch_wave_slices", c_i32), ("fused_sweep", c_i32),
+        ("general", c_i32), ("reserved0", c_i32),
     ]
 
 

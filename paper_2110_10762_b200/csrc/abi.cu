@@ -148,6 +148,8 @@ int pint_op_get_info(const pint_op *op, pint_op_info *info) {
     info->min_pivot = op->plan.min_pivot;
     info->batch_wave_slices = op->batch_wave_slices;
     info->fused_sweep = op->fused_sweep ? 1 : 0;
+    info->general = op->tri_general ? 1 : 0;
+    info->reserved0 = 0;
   }
   return PINT_OK;
 }

@@ -729,8 +729,7 @@ extern "C" int pint_async_domain_launch(int ndom, pint_async_domain **doms, doub
     if (const char *e = getenv("PINT_ASYNC_CLAIM")) S.claim = atoi(e);
     const size_t sm = sizeof(double) * (2 * (size_t)tri1d_nfields(pf.J) * TB + 8 * (size_t)(pf.nW + 1)) + 16 +
                       64 + 32 * 8 * 4;
-    const bool general = pf.tb < pf.T || pf.N % pf.CH != 0 || pf.f_first != 0.0 || pf.f_last != 0.0 || pg.f_first != 0.0 ||
-                         pg.f_last != 0.0 || (!pf.cn && !pf.ccst) || (!pg.cn && !pg.ccst);
+    const bool general = fine->tri_general || coarse->tri_general;
 #define PINT_ASYNC_LAUNCH(CHV, JV, CNF, CNG, GV)                                                          \
   launch_cluster(tri1d_async_kernel<CHV, JV, CNF, CNG, GV>, ncl * CL, TB, CL, sm, s, make_params<CHV>(fine), \
                  make_params<CHV>(coarse), S, (const AsyncDomain *)dd, ndom)

@@ -582,10 +582,8 @@ static void run_kernel_t(TriKind kind, const pint_op *op, int grid_slices, int c
                          int64_t p, const double *prev, double *next, const double *fv, int64_t k,
                          double *deltas, int32_t *nonfinite, int chain) {
   // GENERAL: a partially filled (tail) thread or boundary forcing; the fast path has neither
-  // (backward Euler: the fast path is the constant-coefficient twisted chunk solve)
-  // (and every separator is a real unknown: N a multiple of CH)
-  if (op->plan.tb < op->plan.T || op->plan.N % CH != 0 || op->plan.f_first != 0.0 || op->plan.f_last != 0.0 ||
-      (!CN && !op->plan.ccst))
+  // (backward Euler: the fast path is the constant-coefficient twisted chunk solve); see tri1d_setup
+  if (op->tri_general)
     run_kernel<CH, J, CN, true>(kind, op, grid_slices, cl, s, in, out, stride, lam, gcache, p, prev, next, fv, k,
                                 deltas, nonfinite, chain);
   else
@@ -666,6 +664,13 @@ void tri1d_setup(pint_op *op) {
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 232448;
     op->fused_sweep = need <= (size_t)optin;
   }
+  // the fast kernels need every thread regular, every separator a real unknown
+  // (N a multiple of CH), no boundary forcing and, for backward Euler, a
+  // usable constant-coefficient chunk solve; PINT_TRI_FORCE_GENERAL=1 selects
+  // the exact-pivot kernels regardless (A/B tests)
+  op->tri_general = pl.tb < pl.T || pl.N % pl.CH != 0 || pl.f_first != 0.0 || pl.f_last != 0.0 ||
+                    (!pl.cn && !pl.ccst);
+  if (const char *fg = getenv("PINT_TRI_FORCE_GENERAL")) op->tri_general = op->tri_general || atoi(fg) != 0;
   if (const char *mb = getenv("PINT_TRI_MINB")) op->batch_minb = atoi(mb) == 1 ? 1 : 2;
   if (const char *bc = getenv("PINT_TRI_BATCH_CL")) {
     const int v = atoi(bc);

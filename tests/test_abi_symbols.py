@@ -39,7 +39,7 @@ def test_library_loads_and_binding_is_complete():
     assert set(declared()) <= set(_native.SIGNATURES)
     # struct layout matches the header (8-byte aligned, no implicit padding)
     assert ctypes.sizeof(_native.OpDesc) == 4 * 4 + 8 * 3 + 8 * 3 + 8 * 4 + 8 * 2 + 4 * 2
-    assert ctypes.sizeof(_native.OpInfo) == 8 * 2 + 4 * 6 + 8 * 4 + 4 * 2
+    assert ctypes.sizeof(_native.OpInfo) == 8 * 2 + 4 * 6 + 8 * 4 + 4 * 4
 
 
 def test_library_is_sm100a_code():

@@ -285,3 +285,34 @@ def test_trapezoidal_fine_backward_euler_coarse_large(gpu, n, p):
     assert tr.k_final == ref.k_final and tr.stop_reason == ref.stop_reason
     for k, it in enumerate(tr.iterates):
         assert rel_l2(it.data, ref.iterates[k]) < 1e-9, k
+
+
+@pytest.mark.parametrize("n,steps,slices", [(1024, 100, 16), (4096, 37, 3), (65536, 1000, 4)])
+def test_fast_path_agrees_with_exact_pivot_path_and_truth(gpu, monkeypatch, n, steps, slices):
+    """The backward-Euler fast path (constant-coefficient twisted chunk
+    solve) against the exact-pivot kernels on the same operator
+    (PINT_TRI_FORCE_GENERAL=1 at operator creation) and against the
+    long-double truth: both stay inside the fp64 tolerance and differ from
+    each other by rounding only."""
+    from oracle import heat_oracle as H
+    from oracle.truth import TruthTridiag1D
+    span = 1.0 / 64
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    rng = np.random.default_rng(n)
+    x = np.stack([H.sine_u0_1d(n, 8, seed=s) + 0.01 * rng.standard_normal(n) for s in range(slices)])
+    fast = gpu.backward_euler_propagator(ivp, span, steps)
+    assert not fast.info.general
+    import torch
+    xd = torch.tensor(x, device="cuda")
+    y_fast = fast.apply_batch(xd).cpu().numpy()
+    monkeypatch.setenv("PINT_TRI_FORCE_GENERAL", "1")
+    exact = gpu.backward_euler_propagator(ivp, span, steps)
+    assert exact.info.general
+    y_exact = exact.apply_batch(xd).cpu().numpy()
+    a_d, a_o, c = H.heat1d_coeffs(n)
+    want = TruthTridiag1D(n, a_d, a_o, c, span, steps).apply_batch(x)
+    e_fast, e_exact, e_ab = rel_l2(y_fast, want), rel_l2(y_exact, want), rel_l2(y_fast, y_exact)
+    print(f"n={n} steps={steps}: fast {e_fast:.2e} exact-pivot {e_exact:.2e} fast vs exact-pivot {e_ab:.2e}")
+    tol = 1e-12 if n <= 4096 else 1e-10
+    assert e_fast < tol and e_exact < tol and e_ab < tol
+    assert e_fast < 4 * e_exact + 1e-14

@@ -185,3 +185,50 @@ def test_simulate_async_needs_the_parareal_mapping():
     m = AsyncMapping(1, 1, lambda i, r: r[(0, 1)], {1: ((0, 1),)})
     with pytest.raises(NotImplementedError):
         pb.simulate_async(m, np.zeros((2, 3)), pb.AsyncSchedule(seed=0, delay_bound=0))
+
+
+def test_fast_path_factors_and_dispatch():
+    """The backward-Euler fast path (constant-coefficient twisted chunk solve,
+    csrc/tri1d.cu): closed-form factors satisfy their defining identities and
+    the dispatch falls back to the exact-pivot path where the scheme does not
+    apply (ragged N, boundary forcing, dt far beyond the slowest mode)."""
+    import ctypes
+
+    from paper_2110_10762_b200 import _native as nat
+    lib = nat.load_library()
+
+    def query(n, r, c_first=0.0):
+        h = 1.0 / (n + 1)
+        d = nat.OpDesc()
+        d.ndim, d.rule, d.dtype = 1, 0, nat.PINT_F64
+        d.shape[0] = n
+        d.span, d.steps = r * h * h, 1
+        d.a_diag, d.a_off, d.c_first, d.c_last = -2.0 / (h * h), 1.0 / (h * h), c_first, 0.0
+        usable = ctypes.c_int32(-1)
+        fac = np.zeros(11 + 3 * 16)
+        rc = lib.pint_tri1d_ccst_host(ctypes.byref(d), ctypes.byref(usable), fac.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        return usable.value, fac
+
+    ok, f = query(65536, 67110.9)
+    assert ok == 1
+    mu, kap, kapm, al, be, ga, sAB, sB, nlam, CmAB, CmN = f[:11]
+    lam = -nlam
+    D, E = 1.0 + 2 * 67110.9, -67110.9
+    c = 1.0 / kap
+    assert abs(c * c - D * c + E * E) / (c * c) < 1e-12      # c solves c^2 - D c + E^2 = 0
+    assert abs(lam - (-E / c)) < 1e-15 and abs(mu - lam * lam) < 1e-15
+    assert abs(kapm - 1.0 / (c * (1.0 - mu))) / kapm < 1e-10
+    assert abs(sAB - (1.0 - mu) / (1.0 + lam ** 32)) / sAB < 1e-10
+    assert abs(CmAB - lam ** 16 / (1.0 + lam ** 32)) < 1e-12 and 0.49 < CmAB < 0.5
+    g, rs, ro = f[11:27], f[27:43], f[43:59]
+    assert np.allclose(rs[:15] * ro[:15], 1.0, rtol=1e-15)
+    assert np.allclose(ro[:15], lam ** np.arange(15, 0, -1), rtol=1e-13)
+    assert np.allclose(g[:15], -E * lam ** (2.0 * np.arange(15) - 15), rtol=1e-12)
+    # dispatch
+    assert query(65535, 67110.9)[0] == 0          # N not a multiple of the chunk
+    assert query(1000, 656.6)[0] == 0             # partially filled last thread
+    assert query(1024, 656.6)[0] == 1
+    assert query(1024, 656.6, c_first=1.0)[0] == 0  # boundary forcing
+    assert query(1024, 1e10)[0] == 0              # dt >> slowest mode: exact-pivot path
+    assert query(65536, 1e10)[0] == 1
