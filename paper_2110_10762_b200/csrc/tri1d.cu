@@ -410,7 +410,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   const uint32_t row = smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
   const uint32_t wrow0 = row - (uint32_t)c.lane * RS;  // lane 0's row
   const int64_t wbase = (int64_t)(c.t - c.lane) * CH;  // warp segment start (points)
-  const bool even = (N & 1) == 0;
+  const bool even = !GENERAL || (N & 1) == 0;  // fast path: N is a multiple of CH
   double nanacc = 0.0;
   for (int64_t i = k; i <= p; ++i) {
     {
@@ -420,7 +420,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
         for (int kk = 0; kk < CH / 2; ++kk) {
           const int e = kk * 64 + 2 * c.lane;
           const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
-          if (wbase + e < N) {
+          if (!GENERAL || wbase + e < N) {  // fast path: N is a multiple of CH, every point real
 #pragma unroll
             for (int a = 0; a < 3; ++a) cp_async16(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
           }
@@ -446,6 +446,42 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     __syncwarp();
     const uint32_t r = opaque(row);
     double dm = 0.0;
+    if (!GENERAL) {
+      // fast path: every point of every thread is real (N a multiple of CH);
+      // the F-only choice (warp-uniform) is hoisted out of the point loop.
+      // Same per-point expressions as the general loop below.
+      if (fonly) {
+#pragma unroll
+        for (int j = 0; j < CH; j += 2) {
+          const double g0 = x[j], g1 = x[j + 1];
+          const double v0 = lds_free(r + (uint32_t)j * 8u), v1 = lds_free(r + (uint32_t)(j + 1) * 8u);
+          dm = fmax(dm, fabs(v0 - lds_free(r + (uint32_t)(2 * CH + j) * 8u)));
+          dm = fmax(dm, fabs(v1 - lds_free(r + (uint32_t)(2 * CH + j + 1) * 8u)));
+          nanacc += v0 - v0;
+          nanacc += v1 - v1;
+          x[j] = v0;
+          x[j + 1] = v1;
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
+                       : "memory");
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CH; j += 2) {
+          const double g0 = x[j], g1 = x[j + 1];
+          const double v0 = (g0 + lds_free(r + (uint32_t)j * 8u)) - lds_free(r + (uint32_t)(CH + j) * 8u);
+          const double v1 = (g1 + lds_free(r + (uint32_t)(j + 1) * 8u)) - lds_free(r + (uint32_t)(CH + j + 1) * 8u);
+          dm = fmax(dm, fabs(v0 - lds_free(r + (uint32_t)(2 * CH + j) * 8u)));
+          dm = fmax(dm, fabs(v1 - lds_free(r + (uint32_t)(2 * CH + j + 1) * 8u)));
+          nanacc += v0 - v0;
+          nanacc += v1 - v1;
+          x[j] = v0;
+          x[j + 1] = v1;
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)j * 8u), "d"(v0), "d"(v1) : "memory");
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
+                       : "memory");
+        }
+      }
+    } else {
     double gprev = 0.0, vprev = 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -468,6 +504,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
         gprev = g;
       }
     }
+    }
     __syncwarp();
     {
       double *dsts[2] = {next + i * N + wbase, gcache + i * N + wbase};
@@ -476,7 +513,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
         for (int kk = 0; kk < CH / 2; ++kk) {
           const int e = kk * 64 + 2 * c.lane;
           const uint32_t src = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
-          if (wbase + e < N) {
+          if (!GENERAL || wbase + e < N) {
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
               double2 v2;
