@@ -137,6 +137,7 @@ struct pint_op {
   int batch_wave_slices = 0;  // slices of apply_batch resident at once (0 = unknown)
   int batch_minb = 2;  // CTAs per SM the fine kernel is register-budgeted for (1 or 2)
   bool fused_sweep = true;  // the fused coarse sweep's shared memory fits one CTA
+  bool sweep_defer = false;  // fused sweep: separate result rows fit (stores drained inside the next step's exchange)
   bool tri_general = false;  // runs the exact-pivot (GENERAL) kernels: tail thread, forcing, or no fast path
   // n-D
   int64_t nx = 1, ny = 1, nz = 1;

@@ -377,7 +377,7 @@ template <int CH, int J, bool CN, bool GENERAL>
 __global__ void __launch_bounds__(256, 1)
 tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__restrict__ prev,
                    double *__restrict__ next, const double *__restrict__ fv, double *__restrict__ gcache,
-                   int64_t k, int64_t p, double *deltas, int32_t *nonfinite, int chain_in) {
+                   int64_t k, int64_t p, double *deltas, int32_t *nonfinite, int chain_in, int defer) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -410,6 +410,31 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   const uint32_t row = smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
   const uint32_t wrow0 = row - (uint32_t)c.lane * RS;  // lane 0's row
   const int64_t wbase = (int64_t)(c.t - c.lane) * CH;  // warp segment start (points)
+  // Fast path: when they fit (`defer`), the results (new | G(new)) are staged
+  // in rows of their own (2 CH doubles + 16 B pad) and drained to global
+  // memory one slice later, inside the next coarse step's cluster exchange
+  // (tri_step's shadow hook); otherwise they go through the F / G(old) slots
+  // of the input rows and are drained right after the correction.
+  const uint32_t OS = defer ? (uint32_t)(2 * CH + 2) * 8u : RS;
+  const uint32_t orow = defer ? smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2 +
+                                         (size_t)c.TB * (3 * CH + 2)) + (uint32_t)threadIdx.x * OS
+                              : row;
+  const uint32_t worow0 = orow - (uint32_t)c.lane * OS;
+  auto drain = [&](int64_t islice) {
+    double *dsts[2] = {next + islice * N + wbase, gcache + islice * N + wbase};
+#pragma unroll
+    for (int kk = 0; kk < CH / 2; ++kk) {
+      const int e = kk * 64 + 2 * c.lane;
+      const uint32_t src = worow0 + (uint32_t)(e / CH) * OS + (uint32_t)(e % CH) * 8u;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        double2 v2;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v2.x), "=d"(v2.y) : "r"(src + (uint32_t)(a * CH) * 8u));
+        *reinterpret_cast<double2 *>(dsts[a] + e) = v2;
+      }
+    }
+    __syncwarp();  // the rows are rewritten by the next correction
+  };
   const bool even = !GENERAL || (N & 1) == 0;  // fast path: N is a multiple of CH
   double nanacc = 0.0;
   for (int64_t i = k; i <= p; ++i) {
@@ -439,7 +464,14 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
       cp_async_commit();
     }
     double dprev = 0.0;
-    run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, dpart, &dprev);
+    if (!GENERAL) {
+      auto shadow = [&]() {
+        if (defer && i > k) drain(i - 1);
+      };
+      run_steps<CH, J, CN, GENERAL, decltype(shadow)>(x, P, c, sc, P.steps, dpart, &dprev, shadow);
+    } else {
+      run_steps<CH, J, CN, GENERAL>(x, P, c, sc, P.steps, dpart, &dprev);
+    }
     if (i > k && rank == 0 && threadIdx.x == 0) deltas[i - 1] = dprev;
     const bool fonly = (i == k) ? (delta_in == 0.0) : (dprev == 0.0);
     cp_async_wait_all();
@@ -450,6 +482,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
       // fast path: every point of every thread is real (N a multiple of CH);
       // the F-only choice (warp-uniform) is hoisted out of the point loop.
       // Same per-point expressions as the general loop below.
+      const uint32_t ro = opaque(orow);
       if (fonly) {
 #pragma unroll
         for (int j = 0; j < CH; j += 2) {
@@ -461,7 +494,8 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
           nanacc += v1 - v1;
           x[j] = v0;
           x[j + 1] = v1;
-          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ro + (uint32_t)j * 8u), "d"(v0), "d"(v1) : "memory");
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ro + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
                        : "memory");
         }
       } else {
@@ -476,8 +510,8 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
           nanacc += v1 - v1;
           x[j] = v0;
           x[j + 1] = v1;
-          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)j * 8u), "d"(v0), "d"(v1) : "memory");
-          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(r + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ro + (uint32_t)j * 8u), "d"(v0), "d"(v1) : "memory");
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(ro + (uint32_t)(CH + j) * 8u), "d"(g0), "d"(g1)
                        : "memory");
         }
       }
@@ -506,7 +540,8 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     }
     }
     __syncwarp();
-    {
+    if (!GENERAL && !defer) drain(i);
+    if (GENERAL) {
       double *dsts[2] = {next + i * N + wbase, gcache + i * N + wbase};
       if (even) {
 #pragma unroll
@@ -537,6 +572,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     __syncwarp();  // the rows are refilled by the next slice's cp.async
     dpart = warp_max(dm);
   }
+  if (!GENERAL && defer) drain(p);  // the last slice's results
   if (nanacc != nanacc) bad = true;
   // final reduction for slice p through one more gather round
   {
@@ -607,8 +643,9 @@ static void run_kernel(TriKind kind, const pint_op *op, int grid_slices, int cl,
     }
     case TriKind::Sweep:
       launch_cluster(tri1d_sweep_kernel<CH, J, CN, GENERAL>, cl, TB, cl,
-                     sm + sizeof(double) * (size_t)TB * (3 * CH + 2), s, P, prev, next, fv, gcache, k, p,
-                     deltas, nonfinite, chain);
+                     sm + sizeof(double) * (size_t)TB * ((3 * CH + 2) + (!GENERAL && op->sweep_defer ? 2 * CH + 2 : 0)),
+                     s, P, prev, next, fv, gcache, k, p,
+                     deltas, nonfinite, chain, (!GENERAL && op->sweep_defer) ? 1 : 0);
       break;
   }
 }
@@ -700,6 +737,8 @@ void tri1d_setup(pint_op *op) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 232448;
     op->fused_sweep = need <= (size_t)optin;
+    // result rows of their own (deferred drain, fast kernels only) when they fit too
+    op->sweep_defer = need + sizeof(double) * (size_t)TBs * (2 * pl.CH + 2) <= (size_t)optin;
   }
   // the fast kernels need every thread regular, every separator a real unknown
   // (N a multiple of CH), no boundary forcing and, for backward Euler, a

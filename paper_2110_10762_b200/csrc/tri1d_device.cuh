@@ -222,7 +222,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
 // gP (row 0), lanes 16..31 gH (row 1); lane & 15 = target CTA. With EXTRA the
 // warp-uniform vX goes to row 2 (a max-reduction riding on the exchange).
 template <bool EXTRA>
-__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double vPH, double vX) {
+__device__ __forceinline__ void gather_publish(const StepCtx &c, uint32_t sc, double vPH, double vX) {
   const uint32_t par = sc & 1u;
   const uint32_t stride = (uint32_t)(c.nW + 1);
   const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
@@ -236,9 +236,24 @@ __device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t s
     if (EXTRA && c.lane < 16) st_async_f64(rgb + 2u * stride * 8u + o, vX, rbar);
   }
   if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * (EXTRA ? 3u : 2u) * 8u);
-  mbar_wait_parity(bar, (sc >> 1) & 1u);
-  return gb;
 }
+__device__ __forceinline__ uint32_t gather_wait(const StepCtx &c, uint32_t sc) {
+  const uint32_t par = sc & 1u;
+  mbar_wait_parity(c.mbar + par * 8u, (sc >> 1) & 1u);
+  return c.gbuf + par * 4u * (uint32_t)(c.nW + 1) * 8u;
+}
+template <bool EXTRA>
+__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double vPH, double vX) {
+  gather_publish<EXTRA>(c, sc, vPH, vX);
+  return gather_wait(c, sc);
+}
+
+// Work a caller places between a step's publish and its wait (the exchange is
+// in flight for several hundred cycles): the fused sweep drains the previous
+// slice's results to global memory there.
+struct NoShadow {
+  __device__ __forceinline__ void operator()() const {}
+};
 
 #define TAB(f) lds_free(tab + (uint32_t)(f) * 8u)
 
@@ -268,9 +283,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // returned in *extra_out when WITH_EXTRA. Backward Euler: IN_RAW means the
 // chunk slots hold the raw state (else the pivot-scaled one), OUT_RAW asks for
 // a raw result (else scaled for the next step). The separator is always raw.
-template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA>
+template <int CH, int J, bool CN, bool GENERAL, bool IN_RAW, bool OUT_RAW, bool WITH_EXTRA, typename Shadow = NoShadow>
 __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
-                                         const Hoisted &H, uint32_t sc, double extra_in, double *extra_out) {
+                                         const Hoisted &H, uint32_t sc, double extra_in, double *extra_out,
+                                         const Shadow &shadow = Shadow()) {
   constexpr bool CC = !CN && !GENERAL;  // constant-coefficient twisted chunk solve
   const bool regular = !GENERAL || c.t < P.tb;
   const uint32_t tab = opaque(c.tab);
@@ -342,7 +358,9 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   // 31, lanes 16..31 take gH from lane 0
   const double gPH = shfl_d(c.lane == 31 ? pw : h0, c.lane < 16 ? 31 : 0);
   PHASE(3)
-  const uint32_t gb = opaque(gather_exchange<WITH_EXTRA>(c, sc, gPH, extra_in));
+  gather_publish<WITH_EXTRA>(c, sc, gPH, extra_in);
+  shadow();
+  const uint32_t gb = opaque(gather_wait(c, sc));
   PHASE(4)
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
@@ -432,23 +450,25 @@ __device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *s
 // S implicit steps from a raw state to a raw state; the step counter `sc`
 // drives the double-buffered exchange. With extra_out != nullptr the first
 // step also reduces extra_in (max) over the slice.
-template <int CH, int J, bool CN, bool GENERAL>
+template <int CH, int J, bool CN, bool GENERAL, typename Shadow = NoShadow>
 __device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH> &P, const StepCtx &c,
-                                          uint32_t &sc, int64_t S, double extra_in, double *extra_out) {
+                                          uint32_t &sc, int64_t S, double extra_in, double *extra_out,
+                                          const Shadow &shadow = Shadow()) {
   Hoisted H;
 #pragma unroll
   for (int r = 0; r < HoistCount<GENERAL, CN>::value; ++r) {
     H.a[r] = lds(c.tab + (uint32_t)(TF_PCR_A + r) * 8u);
     H.g[r] = lds(c.tab + (uint32_t)(TF_PCR_G + r) * 8u);
   }
+  // `shadow` runs once, inside the first step's exchange
   if (S == 1) {
-    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, H, sc, extra_in, extra_out);
-    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, H, sc, 0.0, nullptr);
+    if (extra_out) tri_step<CH, J, CN, GENERAL, true, true, true>(x, P, c, H, sc, extra_in, extra_out, shadow);
+    else tri_step<CH, J, CN, GENERAL, true, true, false>(x, P, c, H, sc, 0.0, nullptr, shadow);
     ++sc;
     return;
   }
-  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, H, sc, extra_in, extra_out);
-  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, H, sc, 0.0, nullptr);
+  if (extra_out) tri_step<CH, J, CN, GENERAL, true, false, true>(x, P, c, H, sc, extra_in, extra_out, shadow);
+  else tri_step<CH, J, CN, GENERAL, true, false, false>(x, P, c, H, sc, 0.0, nullptr, shadow);
   ++sc;
   for (int64_t s = 1; s < S - 1; ++s, ++sc)
     tri_step<CH, J, CN, GENERAL, false, false, false>(x, P, c, H, sc, 0.0, nullptr);
