@@ -415,8 +415,8 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   // memory one slice later, inside the next coarse step's cluster exchange
   // (tri_step's shadow hook); otherwise they go through the F / G(old) slots
   // of the input rows and are drained right after the correction.
-  const uint32_t OS = defer ? (uint32_t)(2 * CH + 2) * 8u : RS;
-  const uint32_t orow = defer ? smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2 +
+  const uint32_t OS = (defer & 1) ? (uint32_t)(2 * CH + 2) * 8u : RS;
+  const uint32_t orow = (defer & 1) ? smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2 +
                                          (size_t)c.TB * (3 * CH + 2)) + (uint32_t)threadIdx.x * OS
                               : row;
   const uint32_t worow0 = orow - (uint32_t)c.lane * OS;
@@ -437,36 +437,43 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   };
   const bool even = !GENERAL || (N & 1) == 0;  // fast path: N is a multiple of CH
   double nanacc = 0.0;
-  for (int64_t i = k; i <= p; ++i) {
-    {
-      const double *srcs[3] = {fv + i * N + wbase, gcache + i * N + wbase, prev + i * N + wbase};
-      if (even) {
+  // operands of slice i -> the staging rows (coalesced cp.async, lane l copies
+  // 16 B of the warp's contiguous segment into whichever row owns it)
+  auto prefetch = [&](int64_t i) {
+    const double *srcs[3] = {fv + i * N + wbase, gcache + i * N + wbase, prev + i * N + wbase};
+    if (even) {
 #pragma unroll
-        for (int kk = 0; kk < CH / 2; ++kk) {
-          const int e = kk * 64 + 2 * c.lane;
-          const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
-          if (!GENERAL || wbase + e < N) {  // fast path: N is a multiple of CH, every point real
+      for (int kk = 0; kk < CH / 2; ++kk) {
+        const int e = kk * 64 + 2 * c.lane;
+        const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+        if (!GENERAL || wbase + e < N) {  // fast path: N is a multiple of CH, every point real
 #pragma unroll
-            for (int a = 0; a < 3; ++a) cp_async16(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < CH; ++kk) {
-          const int e = kk * 32 + c.lane;
-          const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
-          if (wbase + e < N) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) cp_async8(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
-          }
+          for (int a = 0; a < 3; ++a) cp_async16(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
         }
       }
-      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < CH; ++kk) {
+        const int e = kk * 32 + c.lane;
+        const uint32_t d = wrow0 + (uint32_t)(e / CH) * RS + (uint32_t)(e % CH) * 8u;
+        if (wbase + e < N) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) cp_async8(d + (uint32_t)(a * CH) * 8u, srcs[a] + e);
+        }
+      }
     }
+    cp_async_commit();
+  };
+  // PINT_SWEEP_PREFETCH_SHADOW (launcher): issue the prefetch inside the coarse
+  // step's exchange as well (fast path)
+  const bool pf_shadow = !GENERAL && (defer & 2);
+  for (int64_t i = k; i <= p; ++i) {
+    if (!pf_shadow) prefetch(i);
     double dprev = 0.0;
     if (!GENERAL) {
       auto shadow = [&]() {
-        if (defer && i > k) drain(i - 1);
+        if (pf_shadow) prefetch(i);
+        if ((defer & 1) && i > k) drain(i - 1);
       };
       run_steps<CH, J, CN, GENERAL, decltype(shadow)>(x, P, c, sc, P.steps, dpart, &dprev, shadow);
     } else {
@@ -540,7 +547,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     }
     }
     __syncwarp();
-    if (!GENERAL && !defer) drain(i);
+    if (!GENERAL && !(defer & 1)) drain(i);
     if (GENERAL) {
       double *dsts[2] = {next + i * N + wbase, gcache + i * N + wbase};
       if (even) {
@@ -572,7 +579,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
     __syncwarp();  // the rows are refilled by the next slice's cp.async
     dpart = warp_max(dm);
   }
-  if (!GENERAL && defer) drain(p);  // the last slice's results
+  if (!GENERAL && (defer & 1)) drain(p);  // the last slice's results
   if (nanacc != nanacc) bad = true;
   // final reduction for slice p through one more gather round
   {
@@ -645,7 +652,8 @@ static void run_kernel(TriKind kind, const pint_op *op, int grid_slices, int cl,
       launch_cluster(tri1d_sweep_kernel<CH, J, CN, GENERAL>, cl, TB, cl,
                      sm + sizeof(double) * (size_t)TB * ((3 * CH + 2) + (!GENERAL && op->sweep_defer ? 2 * CH + 2 : 0)),
                      s, P, prev, next, fv, gcache, k, p,
-                     deltas, nonfinite, chain, (!GENERAL && op->sweep_defer) ? 1 : 0);
+                     deltas, nonfinite, chain,
+                     (!GENERAL && op->sweep_defer) ? (getenv("PINT_SWEEP_PREFETCH_SHADOW") ? 3 : 1) : 0);
       break;
   }
 }
