@@ -571,13 +571,19 @@ static void launch_cluster(Kern kern, int grid, int block, int cl, size_t smem, 
   cfg.blockDim = dim3(block, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (const char *pol = getenv("PINT_CLUSTER_POLICY")) {  // 1 = spread, 2 = load balancing (probe)
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference =
+        atoi(pol) == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+    cfg.numAttrs = 2;
+  }
   PINT_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
