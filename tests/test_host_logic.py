@@ -232,3 +232,22 @@ def test_fast_path_factors_and_dispatch():
     assert query(1024, 656.6, c_first=1.0)[0] == 0  # boundary forcing
     assert query(1024, 1e10)[0] == 0              # dt >> slowest mode: exact-pivot path
     assert query(65536, 1e10)[0] == 1
+
+
+@pytest.mark.parametrize("a_d,a_o", [(-4.0, -1.5), (6.0, 1.0), (6.0, -2.4), (-2.0e4, 0.9e4)])
+def test_fast_path_step_with_either_sign_of_the_coefficients(a_d, a_o):
+    """The C ABI takes any symmetric constant-coefficient operator: positive
+    off-diagonal step-matrix entries (lambda < 0) and negative diagonals run
+    the same fast path; one emulated step solves (I - dt A) x = d."""
+    import tri1d_emulator as EM
+    n = 2048
+    P = EM.export_plan(n, a_d, a_o, 0.0, 0.0, 1.0, 1)
+    assert P["ccst"]
+    d = np.random.default_rng(5).standard_normal(n)
+    x = EM.step(d, P)
+    D, E = P["D"], P["E"]
+    res = D * x
+    res[1:] += E * x[:-1]
+    res[:-1] += E * x[1:]
+    scale = abs(D) * np.abs(x).max() + np.abs(d).max()
+    assert np.max(np.abs(res - d)) / scale < 1e-14
