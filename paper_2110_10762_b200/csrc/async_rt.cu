@@ -220,7 +220,7 @@ tri1d_async_kernel(const __grid_constant__ Tri1DParams<CH> PF, const __grid_cons
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int TB = blockDim.x;
-  const int NF = 17 + 2 * J;
+  const int NF = TRI1D_NF(J);
   const int nW = PF.nW;
   // layout: [tabF][tabG][gather 8(nW+1)][2 mbarriers][ctl 8 x int64][red 128 (delta reduction / board collect)]
   double *tabF = smem;

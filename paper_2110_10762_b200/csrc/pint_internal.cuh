@@ -96,9 +96,14 @@ enum Tri1DField {
   // then TF_HQ / TF_HZ: coefficients of this warp's lane-0 values (y1_0, y0_0)
   //      in the level-2 right-hand side of the previous warp
 };
+//      TF_W1M / TF_V1M: the level-1 spikes of lane - 1 (the left separator's
+//      value is formed by the lane itself; lane 0: 1 / 0, i.e. sl)
 #define TF_HQ(J) (15 + 2 * (J))
 #define TF_HZ(J) (16 + 2 * (J))
-inline int tri1d_nfields(int J) { return 17 + 2 * J; }
+#define TF_W1M(J) (17 + 2 * (J))
+#define TF_V1M(J) (18 + 2 * (J))
+#define TRI1D_NF(J) (19 + 2 * (J))  // odd: the per-thread table rows are bank-conflict free
+inline int tri1d_nfields(int J) { return TRI1D_NF(J); }
 
 struct Tri1DPlan {
   int64_t N = 0;
@@ -109,6 +114,7 @@ struct Tri1DPlan {
   int tb = 0;   // number of regular threads
   double D = 1, E = 0;
   double hq = 0;  // regular separator coupling Ro (fast path's uniform TF_HQ)
+  bool l2win = false;  // level 2 through a 32-column window of R2^{-1} (entries outside cannot change an fp64 result)
   double f_first = 0, f_last = 0;  // per-step rhs forcing at point 0 / N-1 (raw)
   double fq_first = 0, fq_last = 0;  // the same in the pivot-scaled state
   int t_last = 0, l_last = 0;      // thread / slot of point N-1

@@ -285,9 +285,14 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       v1[W][l] = -cr * z30[l];
       TBL(TF_W1, t0 + l) = (double)w1[W][l];
       TBL(TF_V1, t0 + l) = (double)v1[W][l];
+      // the left neighbour's spikes: s_left(lane l + 1) = y1_l + W1_l sl + V1_l sr
+      TBL(TF_W1M(J), t0 + l + 1) = (double)w1[W][l];
+      TBL(TF_V1M(J), t0 + l + 1) = (double)v1[W][l];
     }
     TBL(TF_W1, t0 + 31) = 0.0;
     TBL(TF_V1, t0 + 31) = 1.0;
+    TBL(TF_W1M(J), t0) = 1.0;  // lane 0: s_left = sl
+    TBL(TF_V1M(J), t0) = 0.0;
     TBL(TF_CP, t0 + 31) = (double)RoAt(t0 + 30);
     // level-2 right-hand side of warp W - 1: B = gP_{W-1} - h_W, h_W = cq y1_0 + cz y0_0
     // with the coefficients of column W - 1 (lane 31 of the previous warp)
@@ -318,12 +323,37 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
     tri_solve_ld(nW, r2a.data(), r2b.data(), r2c.data(), z.data());
     for (int row = 0; row < nW; ++row) R2inv[(size_t)row * nW + col] = z[row];
   }
+  // Level-2 window: R2 is strongly diagonally dominant (its couplings are the
+  // chunk Green's function over a whole warp, lam^1024), so its inverse decays
+  // geometrically away from the diagonal. When every entry outside the 32
+  // columns [c0(W), c0(W) + 32), c0(W) = clamp(W - 16, 0, nW - 32), of rows
+  // W - 1 and W is below 2^-64 of the row's largest entry, the dropped terms
+  // cannot change an fp64 dot product, and each lane handles one column
+  // instead of J.
+  P.l2win = false;
+  if (nW > 32) {
+    bool ok = true;
+    for (int W = 0; W < nW && ok; ++W) {
+      const int c0 = std::min(std::max(W - 16, 0), nW - 32);
+      for (int row = std::max(W - 1, 0); row <= W && ok; ++row) {
+        ld mx = 0.0L, out = 0.0L;
+        for (int V = 0; V < nW; ++V) {
+          const ld a = fabsl(R2inv[(size_t)row * nW + V]);
+          mx = std::max(mx, a);
+          if (V < c0 || V >= c0 + 32) out = std::max(out, a);
+        }
+        if (!(out <= mx * 5.4e-20L)) ok = false;
+      }
+    }
+    P.l2win = ok;
+  }
   for (int t = 0; t < T; ++t) {
     const int W = t / 32, lane = t % 32;
+    const int c0 = P.l2win ? std::min(std::max(W - 16, 0), nW - 32) : 0;
     for (int j = 0; j < J; ++j) {
-      const int V = lane + 32 * j;
+      const int V = c0 + lane + 32 * j;
       double prevrow = 0.0, currow = 0.0;
-      if (V < nW) {
+      if (V < nW && !(P.l2win && j > 0)) {
         if (W >= 1) prevrow = (double)R2inv[(size_t)(W - 1) * nW + V];
         currow = (double)R2inv[(size_t)W * nW + V];
       }
@@ -407,7 +437,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   // 32*CH-point segment into whichever row owns it), and writes the new
   // iterate and G(new) back the same way after the correction.
   const uint32_t RS = (uint32_t)(3 * CH + 2) * 8u;  // row stride in bytes
-  const uint32_t row = smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
+  const uint32_t row = smem_u32(smem + TRI1D_NF(J) * c.TB + 8 * (c.nW + 1) + 2) + (uint32_t)threadIdx.x * RS;
   const uint32_t wrow0 = row - (uint32_t)c.lane * RS;  // lane 0's row
   const int64_t wbase = (int64_t)(c.t - c.lane) * CH;  // warp segment start (points)
   // Fast path: when they fit (`defer`), the results (new | G(new)) are staged
@@ -416,7 +446,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   // (tri_step's shadow hook); otherwise they go through the F / G(old) slots
   // of the input rows and are drained right after the correction.
   const uint32_t OS = (defer & 1) ? (uint32_t)(2 * CH + 2) * 8u : RS;
-  const uint32_t orow = (defer & 1) ? smem_u32(smem + (17 + 2 * J) * c.TB + 8 * (c.nW + 1) + 2 +
+  const uint32_t orow = (defer & 1) ? smem_u32(smem + TRI1D_NF(J) * c.TB + 8 * (c.nW + 1) + 2 +
                                          (size_t)c.TB * (3 * CH + 2)) + (uint32_t)threadIdx.x * OS
                               : row;
   const uint32_t worow0 = orow - (uint32_t)c.lane * OS;

@@ -26,6 +26,7 @@ struct Tri1DParams {
   int T, nW, tb;
   int t_last, l_last;
   int has_forcing;
+  int l2win;  // level 2 through the 32-column window (one column per lane)
 };
 
 #define FULLMASK 0xffffffffu
@@ -359,22 +360,42 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double gPH = shfl_d(c.lane == 31 ? pw : h0, c.lane < 16 ? 31 : 0);
   PHASE(3)
   gather_publish<WITH_EXTRA>(c, sc, gPH, extra_in);
+  // while the exchange is in flight: the left neighbour's local value (its
+  // separator is formed by this lane itself after level 2, no shuffle then)
+  double y1m = shfl_up_d(y1, 1);
+  if (c.lane == 0) y1m = 0.0;
   shadow();
   const uint32_t gb = opaque(gather_wait(c, sc));
   PHASE(4)
   const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
   double sl = 0.0, sr = 0.0, ex = 0.0;
+  if (J > 1 && P.l2win) {
+    // one column per lane: the 32-column window of R2^{-1} around the diagonal
+    const int V = min(max(c.Wg - 16, 0), c.nW - 32) + c.lane;
+    const uint32_t o = (uint32_t)V * 8u;
+    const double B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
+    sl = TAB(TF_R2) * B;
+    sr = TAB(TF_R2 + J) * B;
+    if (WITH_EXTRA) {
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int V = c.lane + 32 * j;
-    double B = 0.0;
-    if (V < c.nW) {
-      const uint32_t o = (uint32_t)V * 8u;
-      B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
-      if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 2u * stride8 + o));
+      for (int j = 0; j < J; ++j) {
+        const int Vx = c.lane + 32 * j;
+        if (Vx < c.nW) ex = fmax(ex, lds_free(gb + 2u * stride8 + (uint32_t)Vx * 8u));
+      }
     }
-    sl = fma(TAB(TF_R2 + j), B, sl);
-    sr = fma(TAB(TF_R2 + J + j), B, sr);
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int V = c.lane + 32 * j;
+      double B = 0.0;
+      if (V < c.nW) {
+        const uint32_t o = (uint32_t)V * 8u;
+        B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
+        if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 2u * stride8 + o));
+      }
+      sl = fma(TAB(TF_R2 + j), B, sl);
+      sr = fma(TAB(TF_R2 + J + j), B, sr);
+    }
   }
   // split butterfly: the lower half-warp reduces sl, the upper half sr
   {
@@ -395,8 +416,9 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (WITH_EXTRA) *extra_out = ex;
   // the tables of lane 31 (W1 = 0, V1 = 1, y1 = 0) make its value sr
   const double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
-  double s_left = shfl_up_d(s, 1);
-  if (c.lane == 0) s_left = sl;
+  // the left separator by the same expression the left lane evaluates (lane
+  // 0's table entries 1 / 0 with y1m = 0 make it sl)
+  const double s_left = fma(TAB(TF_V1M(J)), sr, fma(TAB(TF_W1M(J)), sl, y1m));
   PHASE(5)
   x[CH - 1] = s;
   if (CC) {
@@ -428,7 +450,7 @@ __device__ __forceinline__ StepCtx setup_ctx(const Tri1DParams<CH> &P, double *s
   c.t = rank * c.TB + threadIdx.x;
   c.lane = threadIdx.x & 31;
   c.Wg = c.t >> 5;
-  const int NF = 17 + 2 * J;  // odd: the per-thread rows are bank-conflict free
+  const int NF = TRI1D_NF(J);  // odd: the per-thread rows are bank-conflict free
   double *tab = smem;
   for (int f = 0; f < NF; ++f) tab[threadIdx.x * NF + f] = P.table[(size_t)f * P.T + c.t];
   c.tab = smem_u32(tab + threadIdx.x * NF);
@@ -549,6 +571,7 @@ static Tri1DParams<CH> make_params(const pint_op *op) {
   P.steps = pl.steps;
   P.E = pl.E;
   P.hq = pl.hq;
+  P.l2win = pl.l2win ? 1 : 0;
   P.f_first = pl.cn ? pl.f_first : pl.fq_first;
   P.f_last = pl.cn ? pl.f_last : pl.fq_last;
   P.T = pl.T;

@@ -134,19 +134,30 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     Hh = np.append(_fma(hq, y1w[:, 0], hz * y0.reshape(nW, 32)[:, 0]), 0.0)
     sl = np.zeros(T)
     sr = np.zeros(T)
-    for j in range(J):
-        V = lane + 32 * j
-        ok = V < nW
-        Vc = np.minimum(V, nW - 1)
-        B = np.where(ok, pw[Vc] - Hh[np.minimum(V + 1, nW)], 0.0)
-        sl = sl + tab[15 + j] * B
-        sr = sr + tab[15 + J + j] * B
+    # level-2 window (tri1d.cu): the plan zeroes the fields of columns j >= 1
+    # when one 32-column window of R2^{-1} per warp suffices
+    windowed = J > 1 and not tab[15 + 1:15 + J].any() and not tab[15 + J + 1:15 + 2 * J].any()
+    if windowed:
+        Wg = np.arange(T) // 32
+        V = np.minimum(np.maximum(Wg - 16, 0), nW - 32) + lane
+        B = pw[V] - Hh[V + 1]
+        sl = tab[15] * B
+        sr = tab[15 + J] * B
+    else:
+        for j in range(J):
+            V = lane + 32 * j
+            ok = V < nW
+            Vc = np.minimum(V, nW - 1)
+            B = np.where(ok, pw[Vc] - Hh[np.minimum(V + 1, nW)], 0.0)
+            sl = sl + tab[15 + j] * B
+            sr = sr + tab[15 + J + j] * B
     sl = sl.reshape(nW, 32).sum(axis=1).repeat(32)
     sr = sr.reshape(nW, 32).sum(axis=1).repeat(32)
     s = _fma(tab[13], sr, _fma(tab[12], sl, y1))
     s[lane == 31] = sr[lane == 31]
-    s_left = _shfl_up(s, 1)
-    s_left[lane == 0] = sl[lane == 0]
+    y1m = _shfl_up(y1, 1)
+    y1m[lane == 0] = 0.0
+    s_left = _fma(tab[18 + 2 * J], sr, _fma(tab[17 + 2 * J], sl, y1m))
     out = d.copy()
     out[:, CH - 1] = s
     if cc:
