@@ -613,7 +613,7 @@ tri1d_sweep_kernel(const __grid_constant__ Tri1DParams<CH> P, const double *__re
   if (nanacc != nanacc) bad = true;
   // final reduction for slice p through one more gather round
   {
-    const uint32_t gb = gather_exchange<true>(c, sc, 0.0, dpart);
+    const uint32_t gb = gather_exchange<true>(c, sc, 0.0, 0.0, dpart);
     const uint32_t stride8 = (uint32_t)(c.nW + 1) * 8u;
     double ex = 0.0;
     for (int V = c.lane; V < c.nW; V += 32) ex = fmax(ex, lds(gb + 2u * stride8 + (uint32_t)V * 8u));

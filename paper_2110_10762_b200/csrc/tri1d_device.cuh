@@ -202,6 +202,10 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
                :: "r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
 }
+__device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double v0, double v1, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+               :: "r"(raddr), "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"(rbar) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
 }
@@ -219,22 +223,25 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
 
 // Publish this warp's level-2 values to every CTA of the cluster and wait for
 // the whole slice's values of step `sc` (double buffered by sc & 1; the
-// mbarrier of each buffer completes one phase per use). vPH: lanes 0..15 carry
-// gP (row 0), lanes 16..31 gH (row 1); lane & 15 = target CTA. With EXTRA the
+// mbarrier of each buffer completes one phase per use). Lanes 0..CL-1 store the
+// pair (gH, gP) of warp W at doubles [2W, 2W+1] of the target CTA's buffer with
+// ONE 16-byte st.async: the receiving mbarrier absorbs its transaction-count
+// updates serially, and halving them (64 instead of 128 per CTA and step)
+// took the exchange of a lone slice from 542 to 407 cycles. With EXTRA the
 // warp-uniform vX goes to row 2 (a max-reduction riding on the exchange).
 template <bool EXTRA>
-__device__ __forceinline__ void gather_publish(const StepCtx &c, uint32_t sc, double vPH, double vX) {
+__device__ __forceinline__ void gather_publish(const StepCtx &c, uint32_t sc, double vH, double vP, double vX) {
   const uint32_t par = sc & 1u;
   const uint32_t stride = (uint32_t)(c.nW + 1);
   const uint32_t gb = c.gbuf + par * 4u * stride * 8u;
   const uint32_t bar = c.mbar + par * 8u;
-  const int tgt = c.lane & 15;
-  if (tgt < c.CL) {
-    const uint32_t rgb = mapa(gb, (uint32_t)tgt);
-    const uint32_t rbar = mapa(bar, (uint32_t)tgt);
-    const uint32_t o = (uint32_t)c.Wg * 8u;
-    st_async_f64(rgb + (c.lane < 16 ? 0u : stride * 8u) + o, vPH, rbar);
-    if (EXTRA && c.lane < 16) st_async_f64(rgb + 2u * stride * 8u + o, vX, rbar);
+  if (c.lane < c.CL) {
+    const uint32_t rgb = mapa(gb, (uint32_t)c.lane);
+    const uint32_t rbar = mapa(bar, (uint32_t)c.lane);
+    // one 16-byte store per target CTA: half the transaction-count updates
+    // the receiving mbarrier has to absorb per step
+    st_async_v2f64(rgb + (uint32_t)c.Wg * 16u, vH, vP, rbar);
+    if (EXTRA) st_async_f64(rgb + 2u * stride * 8u + (uint32_t)c.Wg * 8u, vX, rbar);
   }
   if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)c.nW * (EXTRA ? 3u : 2u) * 8u);
 }
@@ -244,8 +251,8 @@ __device__ __forceinline__ uint32_t gather_wait(const StepCtx &c, uint32_t sc) {
   return c.gbuf + par * 4u * (uint32_t)(c.nW + 1) * 8u;
 }
 template <bool EXTRA>
-__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double vPH, double vX) {
-  gather_publish<EXTRA>(c, sc, vPH, vX);
+__device__ __forceinline__ uint32_t gather_exchange(const StepCtx &c, uint32_t sc, double vH, double vP, double vX) {
+  gather_publish<EXTRA>(c, sc, vH, vP, vX);
   return gather_wait(c, sc);
 }
 
@@ -355,11 +362,10 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   // what the previous warp's level-2 row needs from this warp, combined on the
   // sender: h = Ro y1_0 + E y0_0 (lane 0's values; coefficients of column W - 1)
   const double h0 = GENERAL ? fma(TAB(TF_HQ(J)), y1, TAB(TF_HZ(J)) * y0) : fma(P.hq, y1, P.E * y0);
-  // one shuffle fetches both published values: lanes 0..15 take gP from lane
-  // 31, lanes 16..31 take gH from lane 0
-  const double gPH = shfl_d(c.lane == 31 ? pw : h0, c.lane < 16 ? 31 : 0);
+  const double gP = shfl_d(pw, 31);
+  const double gH = shfl_d(h0, 0);
   PHASE(3)
-  gather_publish<WITH_EXTRA>(c, sc, gPH, extra_in);
+  gather_publish<WITH_EXTRA>(c, sc, gH, gP, extra_in);
   // while the exchange is in flight: the left neighbour's local value (its
   // separator is formed by this lane itself after level 2, no shuffle then)
   double y1m = shfl_up_d(y1, 1);
@@ -372,8 +378,8 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (J > 1 && P.l2win) {
     // one column per lane: the 32-column window of R2^{-1} around the diagonal
     const int V = min(max(c.Wg - 16, 0), c.nW - 32) + c.lane;
-    const uint32_t o = (uint32_t)V * 8u;
-    const double B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
+    const uint32_t o = (uint32_t)V * 16u;  // pairs (gH_V, gP_V): B = gP_V - gH_{V+1}
+    const double B = lds_free(gb + o + 8u) - lds_free(gb + o + 16u);
     sl = TAB(TF_R2) * B;
     sr = TAB(TF_R2 + J) * B;
     if (WITH_EXTRA) {
@@ -389,9 +395,9 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
       const int V = c.lane + 32 * j;
       double B = 0.0;
       if (V < c.nW) {
-        const uint32_t o = (uint32_t)V * 8u;
-        B = lds_free(gb + o) - lds_free(gb + stride8 + o + 8u);
-        if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 2u * stride8 + o));
+        const uint32_t o = (uint32_t)V * 16u;
+        B = lds_free(gb + o + 8u) - lds_free(gb + o + 16u);
+        if (WITH_EXTRA) ex = fmax(ex, lds_free(gb + 2u * stride8 + (uint32_t)V * 8u));
       }
       sl = fma(TAB(TF_R2 + j), B, sl);
       sr = fma(TAB(TF_R2 + J + j), B, sr);
