@@ -40,7 +40,7 @@ N_MODES = 32
 METRIC = "fine-propagator grid-point updates/s"
 UNIT = "GPt-updates/s"
 BYTES_PER_UPDATE = 16  # one fp64 read + one fp64 write per grid-point update
-FP64_INSTR_PER_UPDATE = 164 / 32  # tri1d_batch_kernel SASS (DFMA+DADD+DMUL) per thread-step / points per thread
+FP64_INSTR_PER_UPDATE = 163 / 32  # tri1d_batch_kernel: executed DFMA+DADD+DMUL per thread-step (SASS, windowed level-2 path) / points per thread
 
 
 def workload_config(n_gpus: int) -> dict:
