@@ -96,13 +96,9 @@ enum Tri1DField {
   // then TF_HQ / TF_HZ: coefficients of this warp's lane-0 values (y1_0, y0_0)
   //      in the level-2 right-hand side of the previous warp
 };
-//      TF_W1M / TF_V1M: the level-1 spikes of lane - 1 (the left separator's
-//      value is formed by the lane itself; lane 0: 1 / 0, i.e. sl)
 #define TF_HQ(J) (15 + 2 * (J))
 #define TF_HZ(J) (16 + 2 * (J))
-#define TF_W1M(J) (17 + 2 * (J))
-#define TF_V1M(J) (18 + 2 * (J))
-#define TRI1D_NF(J) (19 + 2 * (J))  // odd: the per-thread table rows are bank-conflict free
+#define TRI1D_NF(J) (17 + 2 * (J))  // odd: the per-thread table rows are bank-conflict free
 inline int tri1d_nfields(int J) { return TRI1D_NF(J); }
 
 struct Tri1DPlan {

@@ -285,14 +285,9 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       v1[W][l] = -cr * z30[l];
       TBL(TF_W1, t0 + l) = (double)w1[W][l];
       TBL(TF_V1, t0 + l) = (double)v1[W][l];
-      // the left neighbour's spikes: s_left(lane l + 1) = y1_l + W1_l sl + V1_l sr
-      TBL(TF_W1M(J), t0 + l + 1) = (double)w1[W][l];
-      TBL(TF_V1M(J), t0 + l + 1) = (double)v1[W][l];
     }
     TBL(TF_W1, t0 + 31) = 0.0;
     TBL(TF_V1, t0 + 31) = 1.0;
-    TBL(TF_W1M(J), t0) = 1.0;  // lane 0: s_left = sl
-    TBL(TF_V1M(J), t0) = 0.0;
     TBL(TF_CP, t0 + 31) = (double)RoAt(t0 + 30);
     // level-2 right-hand side of warp W - 1: B = gP_{W-1} - h_W, h_W = cq y1_0 + cz y0_0
     // with the coefficients of column W - 1 (lane 31 of the previous warp)
@@ -346,6 +341,7 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       }
     }
     P.l2win = ok;
+    if (const char *e = getenv("PINT_L2WIN")) P.l2win = P.l2win && atoi(e) != 0;  // 0: full rows (A/B switch)
   }
   for (int t = 0; t < T; ++t) {
     const int W = t / 32, lane = t % 32;

@@ -366,10 +366,6 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double gH = shfl_d(h0, 0);
   PHASE(3)
   gather_publish<WITH_EXTRA>(c, sc, gH, gP, extra_in);
-  // while the exchange is in flight: the left neighbour's local value (its
-  // separator is formed by this lane itself after level 2, no shuffle then)
-  double y1m = shfl_up_d(y1, 1);
-  if (c.lane == 0) y1m = 0.0;
   shadow();
   const uint32_t gb = opaque(gather_wait(c, sc));
   PHASE(4)
@@ -422,9 +418,8 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (WITH_EXTRA) *extra_out = ex;
   // the tables of lane 31 (W1 = 0, V1 = 1, y1 = 0) make its value sr
   const double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
-  // the left separator by the same expression the left lane evaluates (lane
-  // 0's table entries 1 / 0 with y1m = 0 make it sl)
-  const double s_left = fma(TAB(TF_V1M(J)), sr, fma(TAB(TF_W1M(J)), sl, y1m));
+  double s_left = shfl_up_d(s, 1);
+  if (c.lane == 0) s_left = sl;
   PHASE(5)
   x[CH - 1] = s;
   if (CC) {

@@ -155,9 +155,8 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     sr = sr.reshape(nW, 32).sum(axis=1).repeat(32)
     s = _fma(tab[13], sr, _fma(tab[12], sl, y1))
     s[lane == 31] = sr[lane == 31]
-    y1m = _shfl_up(y1, 1)
-    y1m[lane == 0] = 0.0
-    s_left = _fma(tab[18 + 2 * J], sr, _fma(tab[17 + 2 * J], sl, y1m))
+    s_left = _shfl_up(s, 1)
+    s_left[lane == 0] = sl[lane == 0]
     out = d.copy()
     out[:, CH - 1] = s
     if cc:
