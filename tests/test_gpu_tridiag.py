@@ -316,3 +316,20 @@ def test_fast_path_agrees_with_exact_pivot_path_and_truth(gpu, monkeypatch, n, s
     tol = 1e-12 if n <= 4096 else 1e-10
     assert e_fast < tol and e_exact < tol and e_ab < tol
     assert e_fast < 4 * e_exact + 1e-14
+
+
+def test_level2_window_does_not_change_the_result(gpu, monkeypatch):
+    """The level-2 window (one column of R2^-1 per lane, csrc/tri1d.cu) drops
+    only terms below 2^-64 of their row's largest: against the full rows
+    (PINT_L2WIN=0 at operator creation) the C2 fine map agrees to rounding
+    (bitwise in practice; reported)."""
+    import torch
+    from oracle import heat_oracle as H
+    n, steps = 65536, 300
+    ivp = gpu.heat1d_system(n, 1.0, 0.0, 0.0, 0.0, 1.0)
+    x = torch.tensor(np.stack([H.sine_u0_1d(n, 32, seed=s) for s in range(3)]), device="cuda")
+    y_win = gpu.backward_euler_propagator(ivp, 1.0 / 64, steps).apply_batch(x).cpu().numpy()
+    monkeypatch.setenv("PINT_L2WIN", "0")
+    y_full = gpu.backward_euler_propagator(ivp, 1.0 / 64, steps).apply_batch(x).cpu().numpy()
+    print("level-2 window vs full rows: bitwise", bool(np.array_equal(y_win, y_full)), "rel", rel_l2(y_win, y_full))
+    assert rel_l2(y_win, y_full) < 1e-14
