@@ -254,7 +254,14 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
     // PCR multipliers (data independent)
     ld pa[31], pb[31], pc[31];
     for (int l = 0; l < 31; ++l) { pa[l] = a[l]; pb[l] = b[l]; pc[l] = c[l]; }
-    for (int r = 0; r < 5; ++r) {
+    // three PCR rounds (distances 1, 2, 4) leave eight independent systems
+    // over the lanes {l, l+8, l+16, l+24} (those <= 30); each is closed by its
+    // dense inverse: y1_l = C0 b_l + C8 b_{l^8} + C16 b_{l^16} + C24 b_{l^24}
+    // (three independent xor shuffles instead of two more dependent rounds).
+    // Table slots: rounds 0..2 in TF_PCR_A/G + r; C0, C8 in TF_PCR_A + 3, + 4;
+    // C16, C24 in TF_PCR_G + 3, + 4 (lane 31: all zero, its value is the
+    // level-2 unknown).
+    for (int r = 0; r < 3; ++r) {
       const int d = 1 << r;
       ld na[31], nb[31], nc[31];
       for (int l = 0; l < 31; ++l) {
@@ -268,8 +275,35 @@ Tri1DPlan tri1d_plan(int64_t N, int CH, double Dd, double Ed, double f_first,
       }
       for (int l = 0; l < 31; ++l) { pa[l] = na[l]; pb[l] = nb[l]; pc[l] = nc[l]; }
     }
-    for (int l = 0; l < 31; ++l) TBL(TF_PCR_INV, t0 + l) = (double)(1.0L / pb[l]);
-    TBL(TF_PCR_INV, t0 + 31) = 0.0;  // lane 31's value is the level-2 unknown: s = 0 + 0 sl + 1 sr
+    for (int g = 0; g < 8; ++g) {
+      int mem[4], nq = 0;
+      for (int q = 0; q < 4; ++q)
+        if (g + 8 * q <= 30) mem[nq++] = g + 8 * q;
+      ld ga[4], gb2[4], gc[4], ginv[4][4];
+      for (int q = 0; q < nq; ++q) {
+        ga[q] = (q > 0) ? pa[mem[q]] : 0.0L;
+        gb2[q] = pb[mem[q]];
+        gc[q] = (q + 1 < nq) ? pc[mem[q]] : 0.0L;
+      }
+      for (int col = 0; col < nq; ++col) {
+        ld e[4] = {0.0L, 0.0L, 0.0L, 0.0L};
+        e[col] = 1.0L;
+        tri_solve_ld(nq, ga, gb2, gc, e);
+        for (int row = 0; row < nq; ++row) ginv[row][col] = e[row];
+      }
+      for (int q = 0; q < nq; ++q) {
+        const int l = mem[q];
+        auto coef = [&](int x) -> double {  // partner l ^ (8 x) = member q ^ x
+          const int qp = q ^ x;
+          return (qp < nq) ? (double)ginv[q][qp] : 0.0;
+        };
+        TBL(TF_PCR_A + 3, t0 + l) = coef(0);
+        TBL(TF_PCR_A + 4, t0 + l) = coef(1);
+        TBL(TF_PCR_G + 3, t0 + l) = coef(2);
+        TBL(TF_PCR_G + 4, t0 + l) = coef(3);
+      }
+    }
+    TBL(TF_PCR_INV, t0 + 31) = 0.0;  // (slot unused by the kernels)
     // spikes: R_CC^{-1} e_0 and e_30
     ld z0[31], z30[31];
     for (int l = 0; l < 31; ++l) { z0[l] = 0; z30[l] = 0; }

@@ -345,18 +345,25 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   if (c.lane == 31) y0n = 0.0;
   double b = dsep - P.E * (ylast + y0n);
   if (GENERAL) b *= TAB(TF_MASK);  // virtual separators (all real on the fast path)
+  constexpr int NH = HoistCount<GENERAL, CN>::value;
 #pragma unroll
-  for (int r = 0; r < 5; ++r) {
+  for (int r = 0; r < 3; ++r) {
     const int d = 1 << r;
     const double bm = shfl_up_d(b, d);
     const double bp = shfl_down_d(b, d);
-    constexpr int NH = HoistCount<GENERAL, CN>::value;
     const double ka = r < NH ? H.a[r] : TAB(TF_PCR_A + r);
     const double kg = r < NH ? H.g[r] : TAB(TF_PCR_G + r);
     b = fma(-kg, bp, fma(-ka, bm, b));
   }
   PHASE(2)
-  const double y1 = b * TAB(TF_PCR_INV);  // lane 31: 0 (its value is the level-2 unknown)
+  // the eight 4-lane systems left by three rounds, closed by their dense
+  // inverses (lane 31: all coefficients 0, its value is the level-2 unknown)
+  const double c0 = 3 < NH ? H.a[3] : TAB(TF_PCR_A + 3);
+  const double c16 = 3 < NH ? H.g[3] : TAB(TF_PCR_G + 3);
+  const double b8 = __shfl_xor_sync(FULLMASK, b, 8);
+  const double b16 = __shfl_xor_sync(FULLMASK, b, 16);
+  const double b24 = __shfl_xor_sync(FULLMASK, b, 24);
+  const double y1 = fma(TAB(TF_PCR_A + 4), b8, c0 * b) + fma(TAB(TF_PCR_G + 4), b24, c16 * b16);
   const double y1_30 = shfl_d(y1, 30);
   const double pw = fma(-TAB(TF_CP), y1_30, b);
   // what the previous warp's level-2 row needs from this warp, combined on the

@@ -55,6 +55,11 @@ def _shfl_up(v, d):
     return out.reshape(-1)
 
 
+def _shfl_xor(v, m):
+    w = v.reshape(-1, 32)
+    return w[:, np.arange(32) ^ m].reshape(-1)
+
+
 def _shfl_down(v, d):
     w = v.reshape(-1, 32)
     out = w.copy()
@@ -119,12 +124,13 @@ def step(x_points: np.ndarray, P: dict) -> np.ndarray:
     y0n = _shfl_down(y0, 1)
     y0n[lane == 31] = 0.0
     b = tab[0] * (dsep - E * (ylast + y0n))
-    for r in range(5):
+    for r in range(3):
         dd = 1 << r
         bm = _shfl_up(b, dd)
         bp = _shfl_down(b, dd)
         b = _fma(-tab[6 + r], bp, _fma(-tab[1 + r], bm, b))
-    y1 = b * tab[11]
+    # dense closure of the eight 4-lane systems (C0, C8 in PCR_A slots 3, 4; C16, C24 in PCR_G slots 3, 4)
+    y1 = _fma(tab[1 + 4], _shfl_xor(b, 8), tab[1 + 3] * b) + _fma(tab[6 + 4], _shfl_xor(b, 24), tab[6 + 3] * _shfl_xor(b, 16))
     y1w = y1.reshape(nW, 32)
     bw = b.reshape(nW, 32)
     pw = _fma(-tab[14].reshape(nW, 32)[:, 31], y1w[:, 30], bw[:, 31])
