@@ -149,15 +149,16 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
 // Per-thread PCR multipliers of the first rounds, held in registers
 // for all steps of an application (the rest are re-read from shared memory
 // every step: the register file holds the state).
-// (four rounds on the fast path - all five measured no faster at 127 registers;
-// none where the general path's extra live values
+// (all five slots on the fast path: three rounds' multipliers and the four
+// closure coefficients, 124 registers; none where the general path's extra live values
 // would otherwise spill under the two-CTAs-per-SM register cap)
 template <bool GENERAL, bool CN>
 struct HoistCount {
-  static constexpr int value = GENERAL ? 0 : (CN ? 2 : 4);
+  static constexpr int value = GENERAL ? 0 : (CN ? 2 : 5);
 };
 struct Hoisted {
   double a[5], g[5];
+  double w1, v1;  // level-1 spikes (fast path only)
 };
 
 struct StepCtx {
@@ -363,7 +364,9 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   const double b8 = __shfl_xor_sync(FULLMASK, b, 8);
   const double b16 = __shfl_xor_sync(FULLMASK, b, 16);
   const double b24 = __shfl_xor_sync(FULLMASK, b, 24);
-  const double y1 = fma(TAB(TF_PCR_A + 4), b8, c0 * b) + fma(TAB(TF_PCR_G + 4), b24, c16 * b16);
+  const double c8 = 4 < NH ? H.a[4] : TAB(TF_PCR_A + 4);
+  const double c24 = 4 < NH ? H.g[4] : TAB(TF_PCR_G + 4);
+  const double y1 = fma(c8, b8, c0 * b) + fma(c24, b24, c16 * b16);
   const double y1_30 = shfl_d(y1, 30);
   const double pw = fma(-TAB(TF_CP), y1_30, b);
   // what the previous warp's level-2 row needs from this warp, combined on the
@@ -424,7 +427,7 @@ __device__ __forceinline__ void tri_step(double (&x)[CH], const Tri1DParams<CH> 
   }
   if (WITH_EXTRA) *extra_out = ex;
   // the tables of lane 31 (W1 = 0, V1 = 1, y1 = 0) make its value sr
-  const double s = fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
+  const double s = NH == 5 ? fma(H.v1, sr, fma(H.w1, sl, y1)) : fma(TAB(TF_V1), sr, fma(TAB(TF_W1), sl, y1));
   double s_left = shfl_up_d(s, 1);
   if (c.lane == 0) s_left = sl;
   PHASE(5)
@@ -489,6 +492,10 @@ __device__ __forceinline__ void run_steps(double (&x)[CH], const Tri1DParams<CH>
   for (int r = 0; r < HoistCount<GENERAL, CN>::value; ++r) {
     H.a[r] = lds(c.tab + (uint32_t)(TF_PCR_A + r) * 8u);
     H.g[r] = lds(c.tab + (uint32_t)(TF_PCR_G + r) * 8u);
+  }
+  if (HoistCount<GENERAL, CN>::value == 5) {
+    H.w1 = lds(c.tab + (uint32_t)TF_W1 * 8u);
+    H.v1 = lds(c.tab + (uint32_t)TF_V1 * 8u);
   }
   // `shadow` runs once, inside the first step's exchange
   if (S == 1) {
