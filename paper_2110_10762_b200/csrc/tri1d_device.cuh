@@ -150,7 +150,8 @@ __device__ __forceinline__ void ccst_back(double (&x)[CH], const CcstFactors<CH>
 // for all steps of an application (the rest are re-read from shared memory
 // every step: the register file holds the state).
 // (all five slots on the fast path: three rounds' multipliers and the four
-// closure coefficients, 124 registers; none where the general path's extra live values
+// closure coefficients plus the lane's two level-1 spikes, 128 registers, no
+// spills; none where the general path's extra live values
 // would otherwise spill under the two-CTAs-per-SM register cap)
 template <bool GENERAL, bool CN>
 struct HoistCount {
